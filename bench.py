@@ -1,0 +1,443 @@
+"""Benchmark of the ARA hot path (BASELINE.json metric: "ms per 1M-trial ARA run; ELT lookups/s and %
+HBM roofline at 1/2/4/8 B200").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config P] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (one process per GPU, NCCL)
+
+A step = one whole ARA run over the config's YET (BASELINE.json configs[1] "paper-shaped" by default:
+1M trials x 1000 events x 16 ELTs): ara_run over every layer (YET stream -> row gathers -> FT1/FT2 ->
+cumulative sum -> FT3 -> YLT), the NCCL YLT all-gather when N > 1, and PML/TVaR at the return periods
+for every layer.  Trials are split in contiguous blocks over the ranks (strong scaling of the fixed
+1M-trial run).  Inputs are device resident (the YET is generated in HBM by the seeded generator)
+when the timed region starts; the ELT tables are built before it (ara_create, timed separately).
+The YET (4 GB) is larger than L2, so no L2 flush is needed between steps; the 128 MB table is meant
+to stay L2-resident (that is the design) -- a cold-L2 figure is reported beside it.
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the reference arm for this
+tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "ms per 1M-trial ARA run; ELT lookups/s and % HBM roofline at 1/2/4/8 B200"
+UNIT = "ms/1M-trial run"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="P")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", type=int, default=None)
+    ap.add_argument("--block", type=int, default=None)
+    ap.add_argument("--bps", type=int, default=None)
+    ap.add_argument("--l2-policy", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cold", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="launch-shape sweep (E8); extra JSON lines to stderr")
+    ap.add_argument("--cpu-sample", type=int, default=65536, help="trials in the cpu_baseline sample")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cold/cpu legs")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ============================================================================ reference arm (CPU oracle)
+def run_reference(args):
+    import oracle
+    from paper_1412_4556_b200 import synth
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = synth.Config.load(args.config)
+    elts = synth.make_elts(cfg)
+    cores = oracle.default_threads()
+    sample = max(1, min(cfg.num_trials, 2048 if cfg.catalog_size <= 2_000_000 else 256))
+    rps = synth.return_periods(sample)
+    times = []
+    for i in range(args.warmup + args.steps):
+        stride = cfg.num_trials // sample
+        trials = (np.arange(sample) * stride + (i % max(1, stride))) % cfg.num_trials
+        yet = synth.make_yet_trials(cfg, trials)
+        t0 = time.perf_counter()
+        y = oracle.ylt_for(cfg, elts, yet, threads=cores)
+        for l in range(len(cfg.layers)):
+            if rps:
+                oracle.pml(y[l], rps)
+                oracle.tvar(y[l], rps)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    per_step = float(np.mean(times))
+    value = per_step * 1e3 * 1e6 / sample
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.description}", "num_trials": cfg.num_trials,
+                   "events_per_trial": [cfg.kmin, cfg.kmax], "layers": len(cfg.layers),
+                   "elts_per_layer": len(cfg.layers[0].elts), "catalog": cfg.catalog_size,
+                   "parallelism": f"oracle threads={cores}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{sample} evenly spaced trials per step of {cfg.num_trials}; value extrapolated "
+                                   f"x{cfg.num_trials / sample:g} to the full run"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ============================================================================ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1412_4556_b200 import ara, synth
+    from paper_1412_4556_b200 import dist as adist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    cfg = synth.Config.load(args.config)
+    L = len(cfg.layers)
+    N = cfg.num_trials
+    t0, t1 = adist.shard_range(N, world, rank)
+    n_local = t1 - t0
+    elts = synth.make_elts(cfg)
+
+    # ---- preprocessing stage: tables (timed separately)
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    ctx = ara.context_for_config(cfg, elts, device=dev.index, stream=stream)
+    create_ms = (time.perf_counter() - c0) * 1e3
+    if args.variant is not None:
+        ctx.ara_set_option(ara.ARA_OPT_VARIANT, args.variant)
+    if args.block is not None:
+        ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, args.block)
+    if args.bps is not None:
+        ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, args.bps)
+    if args.l2_policy is not None:
+        ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, args.l2_policy)
+    info = [ctx.ara_layer_info(l) for l in range(L)]
+
+    # ---- this rank's YET shard, generated in HBM
+    if cfg.fixed_length:
+        K = cfg.kmin
+        q0, q1 = t0 * K, t1 * K
+        offsets_d = None
+        offsets_h = None
+    else:
+        K = 0
+        off = synth.trial_offsets(cfg.seed, N, cfg.kmin, cfg.kmax)
+        q0, q1 = int(off[t0]), int(off[t1])
+        offsets_h = (off[t0:t1 + 1] - np.uint64(q0)).astype(np.uint64)
+        offsets_d = torch.from_numpy(offsets_h.view(np.int64)).to(dev)
+    n_ids = q1 - q0
+    ids = torch.empty(n_ids, dtype=torch.int32, device=dev)
+    synth.yet_ids_device(ids.data_ptr(), cfg.seed, cfg.catalog_size, q0, n_ids, sp)
+    ylt_local = torch.empty((L, n_local), dtype=torch.float64, device=dev)
+    rps = synth.return_periods(N)
+    torch.cuda.synchronize()
+
+    def step(evs=None):
+        if evs is not None:
+            evs[0].record(stream)
+        ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        if evs is not None:
+            evs[1].record(stream)
+        full = adist.gather_ylt(ylt_local, N) if world > 1 else ylt_local
+        res = [ara.ara_pml_tvar(full[l], rps, stream=stream) for l in range(L)] if rps else []
+        return full, res
+
+    # ---- correctness gate + cpu baseline (oracle on a bounded sample of this rank's trials)
+    full, res = step()
+    ctx.ara_check(stream)
+    cpu = None
+    if not args.profile and not args.no_cpu_baseline:
+        import oracle
+        cores = oracle.default_threads()
+        sample = min(n_local, args.cpu_sample)
+        trials = t0 + (np.arange(sample, dtype=np.int64) * n_local) // sample
+        yet_s = synth.make_yet_trials(cfg, trials)
+        c0 = time.perf_counter()
+        y_or = oracle.ylt_for(cfg, elts, yet_s, threads=cores)
+        for l in range(L):
+            if len(synth.return_periods(sample)):
+                oracle.pml(y_or[l], synth.return_periods(sample))
+                oracle.tvar(y_or[l], synth.return_periods(sample))
+        cpu_s = time.perf_counter() - c0
+        got = ylt_local[:, torch.from_numpy(trials - t0).to(dev)].cpu().numpy()
+        tol = np.maximum(1e-6 * np.abs(y_or), 1e-3)
+        bad = int(np.sum(np.abs(got - y_or) > tol))
+        if bad:
+            print(json.dumps({"error": f"parity gate failed: {bad} of {got.size} sampled YLT values outside "
+                                       f"1e-6 rel / 1e-3 abs of the oracle"}), flush=True)
+            sys.exit(3)
+        cpu = {"value": cpu_s * 1e3 * 1e6 / sample, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{sample} evenly spaced trials of rank {rank}'s shard (YLT + PML/TVaR on the sample), "
+                         f"{cpu_s:.2f} s wall; value extrapolated to 1M trials; the same sample gates GPU parity "
+                         f"(0 of {got.size} outside tolerance)",
+               "parity_checked": int(got.size)}
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    # ---- timed region (warm: the table stays L2-resident; the 4 GB YET streams from HBM)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(kev[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = start.elapsed_time(end)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    ctx.ara_check(stream)
+
+    # ---- cold-L2 variant: flush L2 (write 512 MB) before each step, untimed
+    cold_ms = None
+    if not args.profile and not args.no_cold:
+        scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        cold = []
+        for i in range(min(args.steps, 5)):
+            scratch.fill_(i & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            torch.cuda.synchronize()
+            cold.append(a.elapsed_time(b))
+        del scratch
+        ct = torch.tensor([float(np.mean(cold))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ct, op=dist.ReduceOp.MAX)
+        cold_ms = float(ct[0])
+
+    # ---- end to end through the public API with HOST buffers (ara_run_host)
+    e2e = None
+    if not args.profile and not args.no_e2e:
+        host_ids = torch.empty(n_ids, dtype=torch.int32, pin_memory=True)
+        host_ids.copy_(ids)
+        host_ylt = torch.empty((L, n_local), dtype=torch.float64, pin_memory=True)
+        dev_ylt = torch.empty((L, n_local), dtype=torch.float64, device=dev)
+
+        def e2e_step():
+            ctx.ara_run_host(host_ids, host_ylt, offsets=offsets_h, events_per_trial=K, num_trials=n_local,
+                             stream=stream)
+            dev_ylt.copy_(host_ylt, non_blocking=True)  # the metrics read the YLT on the device
+            full = adist.gather_ylt(dev_ylt, N) if world > 1 else dev_ylt
+            return [ara.ara_pml_tvar(full[l], rps, stream=stream) for l in range(L)] if rps else []
+
+        e2e_step()
+        ne = min(args.steps, 5)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(ne):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([a.elapsed_time(b) / ne], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_ms = float(et[0])
+        h2d = n_ids * 4 + (offsets_h.nbytes if offsets_h is not None else 0) + L * n_local * 8
+        d2h = L * n_local * 8 + L * len(rps) * 16
+        e2e = {"value": e2e_ms * 1e6 / N, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e2e_ms, "path": "ara_run_host (pinned host YET streamed in 256 MB batches, copy/compute "
+                                              "overlapped) + ara_pml_tvar"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (ara_layer_kernel, one launch per layer)
+    occ = n_ids  # occurrences on this rank per layer pass
+    row_bytes = [max(32, i["row_stride"]) for i in info]  # sector-rounded row bytes
+    alg_bytes_launch = float(np.mean([occ * (4 + rb) for rb in row_bytes]))
+    launch_ms = kern_ms / L
+    peak, peak_src = peaks()
+    achieved = alg_bytes_launch / (launch_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_{cfg.name}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            pj = json.load(f)
+        if pj.get("variant") == info[0]["variant"]:
+            traffic = pj.get("dram_bytes_per_launch")
+    lookups = float(sum(len(l.elts) for l in cfg.layers)) * (q1 - q0) * world  # approx total when sharded evenly
+    lookups_exact = float(sum(len(l.elts) for l in cfg.layers)) * (
+        N * cfg.kmin if cfg.fixed_length else float(synth.trial_offsets(cfg.seed, N, cfg.kmin, cfg.kmax)[-1]))
+    value = ms_per_step * 1e6 / N
+    n_metric_launches = L * 9 * ((len(rps) + 15) // 16) if rps else 0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.description}", "num_trials": N,
+                   "events_per_trial": [cfg.kmin, cfg.kmax], "layers": L, "elts_per_layer": len(cfg.layers[0].elts),
+                   "catalog": cfg.catalog_size, "entries_per_elt": cfg.entries_per_elt, "regime": cfg.regime,
+                   "parallelism": f"trial-sharded x{world}" + (" + NCCL YLT all-gather" if world > 1 else ""),
+                   "l2": "no flush: inputs (YET %.1f GB) exceed L2; table L2-resident by design (cold_l2_ms beside)"
+                         % (n_ids * 4 / 1e9),
+                   "kernel": info[0]["variant"], "storage": "fp32 ELT losses, fp64 terms/sums/YLT"},
+        "trials_per_s": N / (ms_per_step * 1e-3),
+        "elt_lookups_per_s": lookups_exact / (ms_per_step * 1e-3),
+        "kernel_ms_per_step": kern_ms, "create_ms": create_ms, "cold_l2_ms_per_step": cold_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "ara_layer_kernel",
+                     "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": launch_ms,
+                     "note": f"algorithmic bytes = occurrences x (4 B id + {row_bytes[0]} B sector-rounded row); "
+                             f"peak {peak_src}; the table is L2-resident so this is an effective-bandwidth fraction"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps * (L + n_metric_launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+    if args.sweep:
+        sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
+    """Launch-shape sweep (the paper's threads-per-block study, E8): kernel time per
+    (variant, block threads, blocks per SM, L2 policy)."""
+    import torch
+
+    from paper_1412_4556_b200 import ara
+    nv = info[0]["num_variants"]
+    rb = max(32, info[0]["row_stride"])
+    for v in range(nv):
+        for bt in (128, 256):
+            for bps in (0, 2, 3, 4, 6, 8):
+                for pol in (0, 1, 2):
+                    try:
+                        ctx.ara_set_option(ara.ARA_OPT_VARIANT, v)
+                        ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, bt)
+                        ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, bps)
+                        ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, pol)
+                    except ara.AraError:
+                        continue
+                    for _ in range(2):
+                        ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    for _ in range(5):
+                        ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+                    b.record(stream)
+                    torch.cuda.synchronize()
+                    ms = a.elapsed_time(b) / 5 / L
+                    print(json.dumps({"sweep": ctx.ara_layer_info(0)["variant"], "block": bt, "bps": bps, "l2_policy": pol,
+                                      "launch_ms": ms, "eff_GBps": occ * (4 + rb) / ms / 1e6}), file=sys.stderr, flush=True)
+    ctx.ara_set_option(ara.ARA_OPT_VARIANT, 0)
+    ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, 0)
+    ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, 0)
+    ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, 0)
+
+
+if __name__ == "__main__":
+    main()

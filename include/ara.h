@@ -1,0 +1,186 @@
+/* ara.h -- C ABI of the B200-native Aggregate Risk Analysis (ARA) hot path.
+ *
+ * Source of the method: Varghese & Barker, "Are Clouds Ready to Accelerate Ad hoc Financial
+ * Simulations?", arXiv 1412.4556 (PAPER.md in the reference tree; citations are "PAPER.md:line").
+ *
+ *   Input  YET (Year Event Table), ELTs (Event Loss Tables + FT1), PF (layers + FT2/FT3)
+ *   Output YLT (Year Loss Table), one loss per trial and layer
+ *   For every layer, trial and event occurrence (Algorithm 1):
+ *     1. look the event up in every ELT of the layer (0 if absent)
+ *     2. apply FT1 per ELT, sum across the layer's ELTs
+ *     3. apply the occurrence terms FT2 to that event loss
+ *     4. accumulate over the trial's events and apply the aggregate terms FT3
+ *   Every term is  min(max(x - retention, 0), limit)  (readings c1-c4).
+ *   PML / TVaR are read from the YLT (readings c11-c14).
+ *
+ * Library: libara.so (paper_1412_4556_b200/libara.so), hand-written CUDA for sm_100a only.  No CPU
+ * fallback exists: every compute step runs in the library's kernels.
+ *
+ * Conventions for every entry point:
+ *   - Returns ara_status; never throws, never aborts.  On failure ara_last_error() holds a
+ *     thread-local detail message and no partial object is returned.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is enqueued
+ *     on it; functions say when they synchronise.
+ *   - Arithmetic: ELT losses are fp32 (the stored ground truth); every term, sum and metric is fp64
+ *     (reading c19).
+ */
+#ifndef ARA_H
+#define ARA_H
+#include <stdint.h>
+#if defined(__GNUC__)
+#define ARA_API __attribute__((visibility("default")))
+#else
+#define ARA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ARA_VERSION_MAJOR 0
+#define ARA_VERSION_MINOR 2
+#define ARA_MAX_ELTS_PER_LAYER 128 /* compiled kernel set; more -> ARA_E_UNSUPPORTED (reading c16) */
+#define ARA_MAX_RETURN_PERIODS 256
+
+typedef enum {
+  ARA_OK = 0,
+  ARA_E_ARG = 1,         /* NULL pointer, zero count, bad index, duplicate layer ELT, bad offsets   */
+  ARA_E_RANGE = 2,       /* event id outside [1, catalog_size]; return period outside (1, N]       */
+  ARA_E_DUP = 3,         /* the same event id twice in one ELT                                     */
+  ARA_E_VALUE = 4,       /* loss not finite or <= 0; retention < 0 / non-finite; limit <= 0 / NaN   */
+  ARA_E_NOMEM = 5,       /* device or host allocation failed                                       */
+  ARA_E_CUDA = 6,        /* CUDA runtime error (message from cudaGetErrorString)                   */
+  ARA_E_UNSUPPORTED = 7  /* more than ARA_MAX_ELTS_PER_LAYER ELTs in a layer, not an sm_100 device */
+} ara_status;
+
+/* A (retention, limit) pair: FT1, FT2 or FT3.  retention finite and >= 0; limit > 0, may be +INFINITY. */
+typedef struct {
+  double retention;
+  double limit;
+} ara_terms;
+
+/* One Event Loss Table: event-loss pairs plus its financial terms FT1.
+ * HOST memory; copied by ara_create (caller may free on return).  Entries in any order; ids distinct
+ * and in [1, catalog_size]; losses finite and > 0 (an event absent from the ELT has loss 0). */
+typedef struct {
+  const uint32_t* event_ids;
+  const float* losses;
+  uint64_t num_entries;
+  ara_terms ft1;
+} ara_elt;
+
+/* One Layer: the ELTs it covers (indices into the ara_elt array, in the order the
+ * per-ELT losses are summed) and its occurrence (FT2) and aggregate (FT3) terms.  Programs and the
+ * portfolio are flattened into the list of layers: the paper defines no program-level terms
+ * (reading c18).  HOST memory, copied. */
+typedef struct {
+  const uint32_t* elt_index;
+  uint32_t num_elts; /* 1 .. ARA_MAX_ELTS_PER_LAYER, distinct indices */
+  ara_terms occurrence; /* FT2 */
+  ara_terms aggregate;  /* FT3 */
+} ara_layer;
+
+/* The Year Event Table: trials of event ids, each trial in time order (timestamps
+ * only order events and are not passed, reading c8).  Layout: one contiguous uint32 array, trial-major.
+ *   trial_offsets == NULL : trial t occupies event_ids[t*K .. (t+1)*K), K = events_per_trial
+ *   trial_offsets != NULL : trial t occupies event_ids[off[t] .. off[t+1]); off has num_trials+1
+ *                           non-decreasing entries, off[num_trials] <= num_events.  Empty trials allowed
+ *                           (loss 0, reading c17).
+ * num_events = number of uint32 ids the event_ids buffer holds (bounds every read).
+ * Whether the pointers are host or device memory is fixed by the entry point that takes them. */
+typedef struct {
+  const uint32_t* event_ids;
+  const uint64_t* trial_offsets;
+  uint64_t num_trials;
+  uint64_t num_events;
+  uint32_t events_per_trial;
+} ara_yet;
+
+typedef struct ara_ctx ara_ctx; /* opaque; one per device (rank); not thread-safe, distinct contexts are */
+
+/* Preprocessing stage: validate the ELTs and layers, and build on `device`, for every
+ * layer, its event-major interleaved direct-access table: row e (e = 0..C) holds
+ * the fp32 losses of event e in the layer's ELTs, in layer order, zero where absent; row 0 is all
+ * zero.  Row stride = 4*J bytes rounded up to a power of two when <= 32 B, else to a multiple of
+ * 32 B (ara_table_footprint).  Synchronises `stream` once.  On success *out owns all device memory.
+ * Errors: ARA_E_ARG (NULL / zero counts / bad layer index / duplicate index in a layer),
+ * ARA_E_RANGE (ELT id outside [1, C]), ARA_E_DUP, ARA_E_VALUE, ARA_E_UNSUPPORTED, ARA_E_NOMEM,
+ * ARA_E_CUDA. */
+ARA_API ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_elts, const ara_layer* layers,
+                      uint32_t num_layers, int device, void* stream, ara_ctx** out);
+
+ARA_API void ara_destroy(ara_ctx* ctx); /* NULL is a no-op; synchronises the device before freeing */
+
+/* The analysis stage (Algorithm 1) over a DEVICE-resident YET (borrowed; must stay
+ * alive and unmodified until the work on `stream` completes).  Writes ylt[l * num_trials + t]
+ * (DEVICE, caller-allocated, num_layers * num_trials doubles).  Layer-outer order (one pass over the
+ * YET per layer).  Asynchronous: invalid ids / offsets found by the kernels are
+ * recorded in the context and reported by ara_check (the offending occurrences contribute 0).
+ * Errors (immediate): ARA_E_ARG (NULL, num_events too small for fixed-length trials), ARA_E_CUDA. */
+ARA_API ara_status ara_run(ara_ctx* ctx, const ara_yet* yet, double* ylt, void* stream);
+
+/* End-to-end variant for a HOST YET (pinned memory gives copy/compute overlap; pageable works but
+ * serialises): the YET is streamed to the device in trial batches on an internal copy stream,
+ * overlapped with the analysis of the previous batch, and the YLT is written to HOST ylt_host
+ * ([num_layers][num_trials]).  Synchronous: returns when ylt_host is complete, with the ara_check
+ * result folded in (ARA_E_RANGE / ARA_E_ARG for invalid ids / offsets). */
+ARA_API ara_status ara_run_host(ara_ctx* ctx, const ara_yet* yet, double* ylt_host, void* stream);
+
+/* Synchronise `stream` and report (then clear) invalid input seen by earlier ara_run calls:
+ * ARA_E_RANGE = an event id outside [1, C]; ARA_E_ARG = decreasing or out-of-bounds trial offsets. */
+ARA_API ara_status ara_check(ara_ctx* ctx, void* stream);
+
+/* Probable Maximum Loss and Tail Value-at-Risk of a DEVICE YLT of n values >= 0 at m return periods
+ * (readings c11, c12, c14): k = ceil(n / RP) -- exact integer ceil for integral RP, ceil(x - 1e-9 x),
+ * x = n / RP, otherwise; PML = k-th largest value; TVaR = mean of the k largest.  Computed with a
+ * device MSD radix select on the fp64 bit patterns plus a deterministic fp64 tail sum.  Results to
+ * HOST out arrays of m doubles; synchronises `stream`.
+ * Errors: ARA_E_ARG (NULL, n == 0, m == 0 or m > ARA_MAX_RETURN_PERIODS), ARA_E_RANGE (RP not in
+ * (1, n] or not finite), ARA_E_NOMEM, ARA_E_CUDA. */
+ARA_API ara_status ara_pml_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_out,
+                        double* tvar_out, void* stream);
+ARA_API ara_status ara_pml(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream);
+ARA_API ara_status ara_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream);
+
+/* Host-only memory accounting of one layer's direct-access table: bytes of the
+ * (C+1)-row table and its row stride.  No device needed. */
+ARA_API ara_status ara_table_footprint(uint32_t catalog_size, uint32_t num_elts, uint64_t* bytes, uint32_t* row_stride);
+
+/* Multi-GPU reassembly: copy G padded YLT shards gathered as [G][num_layers][shard_cap] (DEVICE)
+ * into ylt ([num_layers][num_trials], DEVICE), shard g holding trials [starts[g], starts[g+1]).
+ * starts: HOST array of G+1 entries, starts[0] = 0, starts[G] = num_trials, each shard <= shard_cap.
+ * Asynchronous device-to-device copies on `stream`. */
+ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint64_t shard_cap, uint32_t num_layers,
+                       const uint64_t* starts, double* ylt, void* stream);
+
+/* Tuning knobs (launch-shape sweep; L2 policy).  0 = library default.
+ *   ARA_OPT_BLOCK_THREADS   threads per block (multiple of 32, <= 1024)
+ *   ARA_OPT_BLOCKS_PER_SM   resident blocks per SM the persistent grid is sized for
+ *   ARA_OPT_L2_POLICY       0 default (evict_last hints on table rows, evict_first on YET ids),
+ *                           1 no hints, 2 hints + persisting access-policy window on the table
+ *   ARA_OPT_VARIANT         kernel variant index within the J class (ara_variant_count) */
+typedef enum {
+  ARA_OPT_BLOCK_THREADS = 1,
+  ARA_OPT_BLOCKS_PER_SM = 2,
+  ARA_OPT_L2_POLICY = 3,
+  ARA_OPT_VARIANT = 4
+} ara_option;
+ARA_API ara_status ara_set_option(ara_ctx* ctx, ara_option opt, int64_t value);
+ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);
+
+/* Introspection for the bench / tests: bytes of layer l's table, its row stride, number of kernel
+ * variants for its J, and a description of the selected variant (static string). */
+ARA_API ara_status ara_layer_info(ara_ctx* ctx, uint32_t layer, uint64_t* table_bytes, uint32_t* row_stride,
+                          uint32_t* num_variants, const char** variant_name);
+
+/* Test hook: copy row `event` of layer l's table (row_stride bytes) to HOST out.  Synchronous. */
+ARA_API ara_status ara_table_row(ara_ctx* ctx, uint32_t layer, uint32_t event, float* out);
+
+ARA_API const char* ara_status_string(ara_status s);
+ARA_API const char* ara_last_error(void);
+ARA_API uint32_t ara_version(void); /* (major << 16) | minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -23,10 +23,10 @@ extern "C" {
  * stream     cudaStream_t (NULL = legacy default stream).  Asynchronous.
  * Returns 0 on success, 1 on invalid arguments (catalog_size == 0, out == NULL with count > 0),
  * 6 on a CUDA launch error (message via ara_synth_last_error()). */
-int ara_synth_yet_ids(uint32_t* out, uint64_t seed, uint64_t q0, uint64_t count, uint32_t catalog_size,
+__attribute__((visibility("default"))) int ara_synth_yet_ids(uint32_t* out, uint64_t seed, uint64_t q0, uint64_t count, uint32_t catalog_size,
                       void* stream);
 
-const char* ara_synth_last_error(void);
+__attribute__((visibility("default"))) const char* ara_synth_last_error(void);
 
 #ifdef __cplusplus
 }

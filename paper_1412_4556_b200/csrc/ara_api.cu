@@ -1,0 +1,623 @@
+// ara_api.cu -- the C ABI of include/ara.h: validation, the per-layer direct-access tables, kernel
+// dispatch, the end-to-end host path, and the small utilities.  Metrics live in metrics.cu.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ara.h"
+#include "ara_kernel.cuh"
+#include "common.cuh"
+
+namespace ara {
+
+static thread_local char g_err[512] = "";
+
+ara_status set_error(ara_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+ara_status cuda_error(cudaError_t e, const char* what) {
+  return set_error(ARA_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------------------------------ layout
+// Row stride in floats: J rounded up to a power of two when 4J <= 32 B (a row never straddles a
+// 32-B sector), else to a multiple of 8 floats (whole sectors).
+static uint32_t row_floats(uint32_t J) {
+  if (J <= 1) return 1;
+  if (J <= 2) return 2;
+  if (J <= 4) return 4;
+  if (J <= 8) return 8;
+  return (J + 7) / 8 * 8;
+}
+
+// ------------------------------------------------------------------------------------------ variants
+typedef void (*KernelFn)(LayerParams);
+
+struct Variant {
+  uint32_t jpad;
+  int V, NV, G, U;
+  KernelFn fn;
+  const char* name;
+};
+
+#define ARA_VAR(V_, NV_, G_, U_) \
+  {(uint32_t)((V_) * (NV_)), V_, NV_, G_, U_, ara_layer_kernel<V_, NV_, G_, U_>, \
+   "ara_layer_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",U=" #U_ ">"}
+
+// First entry per jpad is the default (chosen from the launch-shape sweep).
+static const Variant kVariants[] = {
+    ARA_VAR(1, 1, 1, 8),  ARA_VAR(1, 1, 1, 16),
+    ARA_VAR(2, 1, 1, 8),  ARA_VAR(2, 1, 1, 16),
+    ARA_VAR(4, 1, 1, 8),  ARA_VAR(4, 1, 1, 16),
+    ARA_VAR(8, 1, 1, 8),  ARA_VAR(8, 1, 1, 4),
+    ARA_VAR(8, 2, 2, 8),  ARA_VAR(8, 2, 2, 4),  ARA_VAR(8, 2, 1, 4), ARA_VAR(8, 2, 2, 16), ARA_VAR(8, 2, 1, 8),
+    ARA_VAR(8, 3, 4, 8),  ARA_VAR(8, 3, 2, 4),
+    ARA_VAR(8, 4, 4, 8),  ARA_VAR(8, 4, 2, 4),
+    ARA_VAR(8, 5, 8, 8),  ARA_VAR(8, 5, 4, 4),
+    ARA_VAR(8, 6, 8, 8),  ARA_VAR(8, 6, 4, 4),
+    ARA_VAR(8, 7, 8, 8),  ARA_VAR(8, 7, 4, 4),
+    ARA_VAR(8, 8, 8, 8),  ARA_VAR(8, 8, 4, 4),
+    ARA_VAR(8, 9, 8, 4),  ARA_VAR(8, 9, 16, 8),
+    ARA_VAR(8, 10, 8, 4), ARA_VAR(8, 10, 16, 8),
+    ARA_VAR(8, 11, 8, 4), ARA_VAR(8, 11, 16, 8),
+    ARA_VAR(8, 12, 8, 4), ARA_VAR(8, 12, 16, 8),
+    ARA_VAR(8, 13, 8, 4), ARA_VAR(8, 13, 16, 8),
+    ARA_VAR(8, 14, 8, 4), ARA_VAR(8, 14, 16, 8),
+    ARA_VAR(8, 15, 8, 4), ARA_VAR(8, 15, 16, 8),
+    ARA_VAR(8, 16, 8, 4), ARA_VAR(8, 16, 16, 8),
+};
+static const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
+static void variants_for(uint32_t jpad, std::vector<const Variant*>& out) {
+  out.clear();
+  for (int i = 0; i < kNumVariants; ++i)
+    if (kVariants[i].jpad == jpad) out.push_back(&kVariants[i]);
+}
+
+// ------------------------------------------------------------------------------------------ context
+struct Layer {
+  uint32_t J = 0, jpad = 0;
+  float* table = nullptr;
+  uint64_t table_bytes = 0;
+  std::vector<const Variant*> variants;
+  double r1[kMaxJ], l1[kMaxJ];
+  double r2 = 0, l2 = 0, r3 = 0, l3 = 0;
+};
+
+}  // namespace ara
+
+struct ara_ctx {
+  int device = 0;
+  int sms = 148;
+  uint32_t C = 0;
+  std::vector<ara::Layer> layers;
+  unsigned* d_err = nullptr;
+  unsigned* h_err = nullptr;  // pinned
+  // options
+  int block_threads = 256;
+  int blocks_per_sm = 0;
+  int l2_policy = 0;
+  int variant = 0;
+  int persist_max = 0, window_max = 0;
+  // end-to-end host path
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  uint32_t* st_ids[2] = {nullptr, nullptr};
+  uint64_t* st_off[2] = {nullptr, nullptr};
+  double* st_ylt[2] = {nullptr, nullptr};
+  uint64_t* h_off[2] = {nullptr, nullptr};  // pinned rebased offsets
+  uint64_t st_cap_ids = 0, st_cap_trials = 0;
+};
+
+namespace ara {
+
+static bool valid_terms(const ara_terms& t) {
+  return isfinite(t.retention) && t.retention >= 0.0 && !isnan(t.limit) && t.limit > 0.0;
+}
+
+static ara_status validate(uint32_t C, const ara_elt* elts, uint32_t num_elts, const ara_layer* layers,
+                           uint32_t num_layers) {
+  if (C == 0) return set_error(ARA_E_ARG, "catalog_size must be >= 1");
+  if (!elts || num_elts == 0) return set_error(ARA_E_ARG, "no ELTs");
+  if (!layers || num_layers == 0) return set_error(ARA_E_ARG, "no layers");
+  std::vector<uint64_t> seen((C + 64ull) / 64, 0);
+  for (uint32_t j = 0; j < num_elts; ++j) {
+    const ara_elt& e = elts[j];
+    if (e.num_entries && (!e.event_ids || !e.losses)) return set_error(ARA_E_ARG, "ELT %u: NULL arrays", j);
+    if (!valid_terms(e.ft1)) return set_error(ARA_E_VALUE, "ELT %u: invalid FT1 terms", j);
+    for (uint64_t i = 0; i < e.num_entries; ++i) {
+      uint32_t id = e.event_ids[i];
+      if (id < 1 || id > C) {
+        for (uint64_t k = 0; k < i; ++k) seen[e.event_ids[k] >> 6] = 0;
+        return set_error(ARA_E_RANGE, "ELT %u entry %llu: event id %u outside [1, %u]", j, (unsigned long long)i, id, C);
+      }
+      float l = e.losses[i];
+      if (!isfinite(l) || !(l > 0.0f)) {
+        for (uint64_t k = 0; k < i; ++k) seen[e.event_ids[k] >> 6] = 0;
+        return set_error(ARA_E_VALUE, "ELT %u entry %llu: loss must be finite and > 0", j, (unsigned long long)i);
+      }
+      uint64_t bit = 1ull << (id & 63);
+      if (seen[id >> 6] & bit) {
+        for (uint64_t k = 0; k < i; ++k) seen[e.event_ids[k] >> 6] = 0;
+        return set_error(ARA_E_DUP, "ELT %u: event id %u appears twice", j, id);
+      }
+      seen[id >> 6] |= bit;
+    }
+    for (uint64_t i = 0; i < e.num_entries; ++i) seen[e.event_ids[i] >> 6] = 0;
+  }
+  for (uint32_t l = 0; l < num_layers; ++l) {
+    const ara_layer& L = layers[l];
+    if (!L.elt_index || L.num_elts == 0) return set_error(ARA_E_ARG, "layer %u: no ELTs", l);
+    if (L.num_elts > kMaxJ)
+      return set_error(ARA_E_UNSUPPORTED, "layer %u: %u ELTs > %d", l, L.num_elts, kMaxJ);
+    for (uint32_t m = 0; m < L.num_elts; ++m) {
+      if (L.elt_index[m] >= num_elts) return set_error(ARA_E_ARG, "layer %u: ELT index %u out of range", l, L.elt_index[m]);
+      for (uint32_t k = 0; k < m; ++k)
+        if (L.elt_index[k] == L.elt_index[m]) return set_error(ARA_E_ARG, "layer %u: ELT %u listed twice", l, L.elt_index[m]);
+    }
+    if (!valid_terms(L.occurrence)) return set_error(ARA_E_VALUE, "layer %u: invalid occurrence terms", l);
+    if (!valid_terms(L.aggregate)) return set_error(ARA_E_VALUE, "layer %u: invalid aggregate terms", l);
+  }
+  return ARA_OK;
+}
+
+// Scatter (event id, loss) pairs into the layer's interleaved table: T[id][col] = loss.
+__global__ void __launch_bounds__(256) scatter_kernel(float* __restrict__ table, uint32_t jpad,
+                                                      const uint32_t* __restrict__ ids,
+                                                      const float* __restrict__ losses,
+                                                      const uint32_t* __restrict__ col, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    table[(uint64_t)ids[i] * jpad + col[i]] = losses[i];
+}
+
+static void destroy_ctx(ara_ctx* c) {
+  if (!c) return;
+  DeviceGuard guard(c->device);
+  cudaDeviceSynchronize();
+  for (auto& L : c->layers) cudaFree(L.table);
+  cudaFree(c->d_err);
+  cudaFreeHost(c->h_err);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c->st_ids[i]);
+    cudaFree(c->st_off[i]);
+    cudaFree(c->st_ylt[i]);
+    cudaFreeHost(c->h_off[i]);
+    if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+    if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  delete c;
+}
+
+static const Variant* pick(const ara_ctx* c, const Layer& L) {
+  int v = c->variant;
+  if (v < 0 || v >= (int)L.variants.size()) v = 0;
+  return L.variants[v];
+}
+
+static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, const uint64_t* offsets,
+                               uint64_t num_trials, uint64_t num_events, uint32_t K, double* ylt,
+                               cudaStream_t stream) {
+  if (num_trials == 0) return ARA_OK;
+  const Variant* var = pick(c, L);
+  LayerParams p;
+  memset(&p, 0, sizeof p);
+  p.table = L.table;
+  p.ids = ids;
+  p.offsets = offsets;
+  p.num_trials = num_trials;
+  p.num_events = num_events;
+  p.K = K;
+  p.C = c->C;
+  p.jpad = L.jpad;
+  p.l2_hints = c->l2_policy == 1 ? 0u : 1u;
+  p.ylt = ylt;
+  p.err = c->d_err;
+  p.r2 = L.r2;
+  p.l2 = L.l2;
+  p.r3 = L.r3;
+  p.l3 = L.l3;
+  for (int j = 0; j < kMaxJ; ++j) {
+    p.r1[j] = L.r1[j];
+    p.l1[j] = L.l1[j];
+  }
+  int bps = c->blocks_per_sm;
+  if (bps <= 0) {
+    ARA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)var->fn, c->block_threads, 0));
+    if (bps < 1) bps = 1;
+  }
+  uint64_t warps_per_block = c->block_threads / 32;
+  uint64_t blocks = (uint64_t)c->sms * bps;
+  uint64_t need = (num_trials + warps_per_block - 1) / warps_per_block;
+  if (blocks > need) blocks = need;
+
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(c->block_threads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (c->l2_policy == 2 && c->window_max > 0) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = L.table;
+    size_t bytes = std::min<size_t>(L.table_bytes, (size_t)c->window_max);
+    attr[0].val.accessPolicyWindow.num_bytes = bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)c->persist_max / (double)bytes);
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  ARA_CUDA(cudaLaunchKernelEx(&cfg, var->fn, p));
+  return ARA_OK;
+}
+
+static ara_status run_layers(ara_ctx* c, const uint32_t* ids, const uint64_t* offsets, uint64_t num_trials,
+                             uint64_t num_events, uint32_t K, double* ylt, uint64_t ld, cudaStream_t s) {
+  for (size_t l = 0; l < c->layers.size(); ++l) {
+    ara_status st = launch_layer(c, c->layers[l], ids, offsets, num_trials, num_events, K, ylt + l * ld, s);
+    if (st) return st;
+  }
+  return ARA_OK;
+}
+
+static ara_status check_yet(const ara_yet* y) {
+  if (!y) return set_error(ARA_E_ARG, "yet is NULL");
+  if (y->num_trials == 0) return ARA_OK;
+  if (!y->trial_offsets) {
+    if (y->events_per_trial > 0 && !y->event_ids) return set_error(ARA_E_ARG, "event_ids is NULL");
+    unsigned __int128 need = (unsigned __int128)y->num_trials * y->events_per_trial;
+    if (need > y->num_events) return set_error(ARA_E_ARG, "num_events < num_trials * events_per_trial");
+  } else if (y->num_events > 0 && !y->event_ids) {
+    return set_error(ARA_E_ARG, "event_ids is NULL");
+  }
+  return ARA_OK;
+}
+
+static ara_status take_err(ara_ctx* c, cudaStream_t s) {
+  ARA_CUDA(cudaMemcpyAsync(c->h_err, c->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  ARA_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(unsigned), s));
+  ARA_CUDA(cudaStreamSynchronize(s));
+  unsigned e = *c->h_err;
+  if (e & 1u) return set_error(ARA_E_RANGE, "YET contains an event id outside [1, %u]", c->C);
+  if (e & 2u) return set_error(ARA_E_ARG, "YET trial offsets decrease or exceed num_events");
+  return ARA_OK;
+}
+
+}  // namespace ara
+
+using namespace ara;
+
+extern "C" {
+
+ara_status ara_table_footprint(uint32_t catalog_size, uint32_t num_elts, uint64_t* bytes, uint32_t* row_stride) {
+  if (catalog_size == 0 || num_elts == 0 || (!bytes && !row_stride)) return set_error(ARA_E_ARG, "invalid argument");
+  uint32_t jp = row_floats(num_elts);
+  if (bytes) *bytes = ((uint64_t)catalog_size + 1) * jp * sizeof(float);
+  if (row_stride) *row_stride = jp * (uint32_t)sizeof(float);
+  return ARA_OK;
+}
+
+ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_elts, const ara_layer* layers,
+                      uint32_t num_layers, int device, void* stream, ara_ctx** out) {
+  if (!out) return set_error(ARA_E_ARG, "out is NULL");
+  *out = nullptr;
+  ara_status st = validate(catalog_size, elts, num_elts, layers, num_layers);
+  if (st) return st;
+  int ndev = 0;
+  ARA_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return set_error(ARA_E_ARG, "device %d not present", device);
+  cudaDeviceProp prop;
+  ARA_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return set_error(ARA_E_UNSUPPORTED, "libara is built for sm_100a; device %d is sm_%d%d", device, prop.major, prop.minor);
+  DeviceGuard guard(device);
+  cudaStream_t s = (cudaStream_t)stream;
+
+  ara_ctx* c = new (std::nothrow) ara_ctx();
+  if (!c) return set_error(ARA_E_NOMEM, "host allocation failed");
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  c->C = catalog_size;
+  cudaDeviceGetAttribute(&c->persist_max, cudaDevAttrMaxPersistingL2CacheSize, device);
+  cudaDeviceGetAttribute(&c->window_max, cudaDevAttrMaxAccessPolicyWindowSize, device);
+
+#define FAIL(x)          \
+  do {                   \
+    ara_status _s = (x); \
+    destroy_ctx(c);      \
+    return _s;           \
+  } while (0)
+#define CK(call)                                             \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) FAIL(cuda_error(_e, #call));      \
+  } while (0)
+
+  CK(cudaMalloc(&c->d_err, sizeof(unsigned)));
+  CK(cudaMallocHost(&c->h_err, sizeof(unsigned)));
+  CK(cudaMemsetAsync(c->d_err, 0, sizeof(unsigned), s));
+
+  c->layers.resize(num_layers);
+  std::vector<uint32_t> h_ids, h_col;
+  std::vector<float> h_loss;
+  uint32_t* d_ids = nullptr;
+  uint32_t* d_col = nullptr;
+  float* d_loss = nullptr;
+  for (uint32_t l = 0; l < num_layers; ++l) {
+    Layer& L = c->layers[l];
+    const ara_layer& in = layers[l];
+    L.J = in.num_elts;
+    L.jpad = row_floats(L.J);
+    variants_for(L.jpad, L.variants);
+    if (L.variants.empty()) FAIL(set_error(ARA_E_UNSUPPORTED, "no kernel for row width %u", L.jpad));
+    for (int j = 0; j < kMaxJ; ++j) {
+      L.r1[j] = 0.0;
+      L.l1[j] = INFINITY;
+    }
+    for (uint32_t m = 0; m < L.J; ++m) {
+      L.r1[m] = elts[in.elt_index[m]].ft1.retention;
+      L.l1[m] = elts[in.elt_index[m]].ft1.limit;
+    }
+    L.r2 = in.occurrence.retention;
+    L.l2 = in.occurrence.limit;
+    L.r3 = in.aggregate.retention;
+    L.l3 = in.aggregate.limit;
+    L.table_bytes = ((uint64_t)catalog_size + 1) * L.jpad * sizeof(float);
+    if (cudaMalloc(&L.table, L.table_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      FAIL(set_error(ARA_E_NOMEM, "table of %llu bytes for layer %u", (unsigned long long)L.table_bytes, l));
+    }
+    CK(cudaMemsetAsync(L.table, 0, L.table_bytes, s));
+    h_ids.clear();
+    h_col.clear();
+    h_loss.clear();
+    for (uint32_t m = 0; m < L.J; ++m) {
+      const ara_elt& e = elts[in.elt_index[m]];
+      h_ids.insert(h_ids.end(), e.event_ids, e.event_ids + e.num_entries);
+      h_loss.insert(h_loss.end(), e.losses, e.losses + e.num_entries);
+      h_col.insert(h_col.end(), e.num_entries, m);
+    }
+    uint64_t n = h_ids.size();
+    if (n) {
+      CK(cudaMalloc(&d_ids, n * 4));
+      CK(cudaMalloc(&d_col, n * 4));
+      CK(cudaMalloc(&d_loss, n * 4));
+      CK(cudaMemcpyAsync(d_ids, h_ids.data(), n * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(d_col, h_col.data(), n * 4, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(d_loss, h_loss.data(), n * 4, cudaMemcpyHostToDevice, s));
+      uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)c->sms * 8);
+      scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(L.table, L.jpad, d_ids, d_loss, d_col, n);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(s));  // host staging vectors are reused for the next layer
+      cudaFree(d_ids);
+      cudaFree(d_col);
+      cudaFree(d_loss);
+      d_ids = nullptr;
+      d_col = nullptr;
+      d_loss = nullptr;
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+#undef CK
+#undef FAIL
+  *out = c;
+  return ARA_OK;
+}
+
+void ara_destroy(ara_ctx* ctx) { destroy_ctx(ctx); }
+
+ara_status ara_run(ara_ctx* c, const ara_yet* yet, double* ylt, void* stream) {
+  if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
+  ara_status st = check_yet(yet);
+  if (st) return st;
+  if (yet->num_trials == 0) return ARA_OK;
+  if (!ylt) return set_error(ARA_E_ARG, "ylt is NULL");
+  DeviceGuard guard(c->device);
+  return run_layers(c, yet->event_ids, yet->trial_offsets, yet->num_trials, yet->num_events,
+                    yet->events_per_trial, ylt, yet->num_trials, (cudaStream_t)stream);
+}
+
+ara_status ara_check(ara_ctx* c, void* stream) {
+  if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
+  DeviceGuard guard(c->device);
+  return take_err(c, (cudaStream_t)stream);
+}
+
+ara_status ara_run_host(ara_ctx* c, const ara_yet* yet, double* ylt_host, void* stream) {
+  if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
+  ara_status st = check_yet(yet);
+  if (st) return st;
+  if (yet->num_trials == 0) return ARA_OK;
+  if (!ylt_host) return set_error(ARA_E_ARG, "ylt_host is NULL");
+  DeviceGuard guard(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t N = yet->num_trials;
+  const uint64_t L = c->layers.size();
+  const uint32_t K = yet->events_per_trial;
+  const uint64_t* hoff = yet->trial_offsets;
+  if (hoff) {  // host offsets: validate here (the device copy is rebased per batch)
+    if (hoff[N] > yet->num_events) return set_error(ARA_E_ARG, "trial offsets exceed num_events");
+    for (uint64_t t = 0; t < N; ++t)
+      if (hoff[t + 1] < hoff[t]) return set_error(ARA_E_ARG, "trial offsets decrease at trial %llu", (unsigned long long)t);
+  }
+  // staging: 2 x 256 MB of ids, batches of whole trials
+  const uint64_t cap_ids = 64ull << 20;
+  const uint64_t cap_trials = hoff ? (1ull << 20) : std::max<uint64_t>(1, K ? cap_ids / K : (1ull << 20));
+  if (!c->copy_stream) ARA_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    if (!c->ev_copied[i]) ARA_CUDA(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+    if (!c->ev_done[i]) ARA_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+  }
+  if (c->st_cap_ids < cap_ids || c->st_cap_trials < cap_trials) {
+    ARA_CUDA(cudaDeviceSynchronize());
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(c->st_ids[i]);
+      cudaFree(c->st_off[i]);
+      cudaFree(c->st_ylt[i]);
+      cudaFreeHost(c->h_off[i]);
+      c->st_ids[i] = nullptr;
+      c->st_off[i] = nullptr;
+      c->st_ylt[i] = nullptr;
+      c->h_off[i] = nullptr;
+      c->st_cap_ids = c->st_cap_trials = 0;
+      if (cudaMalloc(&c->st_ids[i], cap_ids * 4) != cudaSuccess || cudaMalloc(&c->st_off[i], (cap_trials + 1) * 8) != cudaSuccess ||
+          cudaMalloc(&c->st_ylt[i], cap_trials * L * 8) != cudaSuccess ||
+          cudaMallocHost(&c->h_off[i], (cap_trials + 1) * 8) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(ARA_E_NOMEM, "staging buffers");
+      }
+    }
+    c->st_cap_ids = cap_ids;
+    c->st_cap_trials = cap_trials;
+  }
+  ARA_CUDA(cudaEventRecord(c->ev_done[0], s));
+  ARA_CUDA(cudaEventRecord(c->ev_done[1], s));
+  uint64_t t0 = 0;
+  int b = 0;
+  while (t0 < N) {
+    // batch [t0, t1): as many whole trials as fit the staging buffer
+    uint64_t t1, q0, q1;
+    if (hoff) {
+      t1 = t0 + 1;
+      while (t1 < N && t1 - t0 < cap_trials && hoff[t1 + 1] - hoff[t0] <= cap_ids) ++t1;
+      q0 = hoff[t0];
+      q1 = hoff[t1];
+      if (q1 - q0 > cap_ids) return set_error(ARA_E_UNSUPPORTED, "a single trial exceeds the staging buffer");
+    } else {
+      t1 = std::min(N, t0 + cap_trials);
+      q0 = t0 * K;
+      q1 = t1 * K;
+    }
+    const int i = b & 1;
+    ARA_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_done[i], 0));
+    if (q1 > q0)
+      ARA_CUDA(cudaMemcpyAsync(c->st_ids[i], yet->event_ids + q0, (q1 - q0) * 4, cudaMemcpyHostToDevice, c->copy_stream));
+    if (hoff) {
+      ARA_CUDA(cudaEventSynchronize(c->ev_done[i]));  // h_off[i] may still be in flight from batch b-2
+      for (uint64_t t = t0; t <= t1; ++t) c->h_off[i][t - t0] = hoff[t] - q0;
+      ARA_CUDA(cudaMemcpyAsync(c->st_off[i], c->h_off[i], (t1 - t0 + 1) * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    }
+    ARA_CUDA(cudaEventRecord(c->ev_copied[i], c->copy_stream));
+    ARA_CUDA(cudaStreamWaitEvent(s, c->ev_copied[i], 0));
+    st = run_layers(c, c->st_ids[i], hoff ? c->st_off[i] : nullptr, t1 - t0, q1 - q0, K, c->st_ylt[i], t1 - t0, s);
+    if (st) return st;
+    for (uint64_t l = 0; l < L; ++l)
+      ARA_CUDA(cudaMemcpyAsync(ylt_host + l * N + t0, c->st_ylt[i] + l * (t1 - t0), (t1 - t0) * 8,
+                               cudaMemcpyDeviceToHost, s));
+    ARA_CUDA(cudaEventRecord(c->ev_done[i], s));
+    t0 = t1;
+    ++b;
+  }
+  return take_err(c, s);
+}
+
+ara_status ara_unshard(const double* gathered, uint32_t G, uint64_t cap, uint32_t L, const uint64_t* starts,
+                       double* ylt, void* stream) {
+  if (!gathered || !starts || !ylt || G == 0 || L == 0) return set_error(ARA_E_ARG, "invalid argument");
+  if (starts[0] != 0) return set_error(ARA_E_ARG, "starts[0] must be 0");
+  const uint64_t N = starts[G];
+  for (uint32_t g = 0; g < G; ++g)
+    if (starts[g + 1] < starts[g] || starts[g + 1] - starts[g] > cap)
+      return set_error(ARA_E_ARG, "shard %u does not fit shard_cap", g);
+  for (uint32_t g = 0; g < G; ++g) {
+    uint64_t cnt = starts[g + 1] - starts[g];
+    if (!cnt) continue;
+    ARA_CUDA(cudaMemcpy2DAsync(ylt + starts[g], N * 8, gathered + (uint64_t)g * L * cap, cap * 8, cnt * 8, L,
+                               cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  }
+  return ARA_OK;
+}
+
+ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
+  if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
+  switch (opt) {
+    case ARA_OPT_BLOCK_THREADS:
+      if (v == 0) v = 256;
+      if (v < 32 || v > 256 || v % 32) return set_error(ARA_E_ARG, "block threads must be a multiple of 32 in [32, 256]");
+      c->block_threads = (int)v;
+      return ARA_OK;
+    case ARA_OPT_BLOCKS_PER_SM:
+      if (v < 0 || v > 32) return set_error(ARA_E_ARG, "blocks per SM in [0, 32]");
+      c->blocks_per_sm = (int)v;
+      return ARA_OK;
+    case ARA_OPT_L2_POLICY:
+      if (v < 0 || v > 2) return set_error(ARA_E_ARG, "L2 policy in {0, 1, 2}");
+      if (v == 2) {
+        DeviceGuard guard(c->device);
+        ARA_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)c->persist_max));
+      }
+      c->l2_policy = (int)v;
+      return ARA_OK;
+    case ARA_OPT_VARIANT:
+      if (v < 0) return set_error(ARA_E_ARG, "variant >= 0");
+      for (auto& L : c->layers)
+        if (v >= (int64_t)L.variants.size()) return set_error(ARA_E_ARG, "variant %lld not available", (long long)v);
+      c->variant = (int)v;
+      return ARA_OK;
+  }
+  return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
+}
+
+ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
+  if (!c || !v) return set_error(ARA_E_ARG, "NULL argument");
+  switch (opt) {
+    case ARA_OPT_BLOCK_THREADS: *v = c->block_threads; return ARA_OK;
+    case ARA_OPT_BLOCKS_PER_SM: *v = c->blocks_per_sm; return ARA_OK;
+    case ARA_OPT_L2_POLICY: *v = c->l2_policy; return ARA_OK;
+    case ARA_OPT_VARIANT: *v = c->variant; return ARA_OK;
+  }
+  return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
+}
+
+ara_status ara_layer_info(ara_ctx* c, uint32_t layer, uint64_t* table_bytes, uint32_t* row_stride,
+                          uint32_t* num_variants, const char** variant_name) {
+  if (!c || layer >= c->layers.size()) return set_error(ARA_E_ARG, "invalid context or layer");
+  const Layer& L = c->layers[layer];
+  if (table_bytes) *table_bytes = L.table_bytes;
+  if (row_stride) *row_stride = L.jpad * 4;
+  if (num_variants) *num_variants = (uint32_t)L.variants.size();
+  if (variant_name) *variant_name = pick(c, L)->name;
+  return ARA_OK;
+}
+
+ara_status ara_table_row(ara_ctx* c, uint32_t layer, uint32_t event, float* out) {
+  if (!c || !out || layer >= c->layers.size()) return set_error(ARA_E_ARG, "invalid argument");
+  if (event > c->C) return set_error(ARA_E_RANGE, "event %u > catalog size %u", event, c->C);
+  DeviceGuard guard(c->device);
+  const Layer& L = c->layers[layer];
+  ARA_CUDA(cudaMemcpy(out, L.table + (uint64_t)event * L.jpad, L.jpad * 4, cudaMemcpyDeviceToHost));
+  return ARA_OK;
+}
+
+const char* ara_status_string(ara_status s) {
+  switch (s) {
+    case ARA_OK: return "ARA_OK";
+    case ARA_E_ARG: return "ARA_E_ARG";
+    case ARA_E_RANGE: return "ARA_E_RANGE";
+    case ARA_E_DUP: return "ARA_E_DUP";
+    case ARA_E_VALUE: return "ARA_E_VALUE";
+    case ARA_E_NOMEM: return "ARA_E_NOMEM";
+    case ARA_E_CUDA: return "ARA_E_CUDA";
+    case ARA_E_UNSUPPORTED: return "ARA_E_UNSUPPORTED";
+  }
+  return "ARA_E_UNKNOWN";
+}
+
+const char* ara_last_error(void) { return g_err; }
+
+uint32_t ara_version(void) { return (ARA_VERSION_MAJOR << 16) | ARA_VERSION_MINOR; }
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+// ara_kernel.cuh -- the ARA hot path on sm_100a: YET stream -> direct-access row gather -> FT1 / sum /
+// FT2 -> per-trial cumulative sum -> FT3 -> YLT.  One launch per layer (Algorithm 1 is layer-outer,
+// PAPER.md:104-105).
+//
+// Mapping (B200-first, not the paper's one-thread-per-trial of PAPER.md:199):
+//   * one WARP per trial, persistent grid-stride loop over trials;
+//   * the warp is split into RG = 32/G row groups of G lanes; a row group owns one event occurrence
+//     at a time and its G lanes fetch that event's table row together (row = the event's losses in
+//     all J ELTs of the layer, event-major interleaved: "ELTs combined as a single
+//     table"), each lane one V-float vector (V = 8 -> one 256-bit LDG = one 32-B sector);
+//     so a 64-B row (J = 16) is one L1 wavefront for 2 lanes instead of 2 wavefronts for 1 lane;
+//   * each row group handles U occurrences per iteration, so a warp has 32/G*U rows in flight;
+//   * FT1 is applied in fp64 only to entries whose fp32 loss is non-zero: an absent event has loss 0
+//     and clamp(0; R>=0, L) = +0 exactly (reading c9), so skipping it is exact, not an approximation;
+//   * the per-row partial sums of the G lanes are combined with xor-shuffles, FT2 is applied, and the
+//     group leader accumulates the occurrence-net loss; the trial's cumulative sum S_n is the
+//     warp-shuffle sum of the leaders' running sums (the YLT needs only the last prefix);
+//   * terms (FT1 per ELT, FT2, FT3) arrive as kernel parameters -- the constant bank, as the paper
+//     keeps terms in constant memory; FT1 is staged into shared memory so a lane can
+//     index it by its entry.
+// Cache policy: table rows are loaded L1::no_allocate with an L2 evict_last policy (the table is the
+// re-used working set); YET ids are streamed with an L2 evict_first policy.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ara {
+
+constexpr int kMaxJ = 128;  // ARA_MAX_ELTS_PER_LAYER
+
+struct LayerParams {
+  const float* table;        // (C+1) x jpad fp32, row 0 zero
+  const uint32_t* ids;       // YET event ids (device)
+  const uint64_t* offsets;   // [num_trials+1] or nullptr
+  uint64_t num_trials;
+  uint64_t num_events;       // ids buffer length (bounds every read)
+  uint32_t K;                // events per trial when offsets == nullptr
+  uint32_t C;                // catalogue size
+  uint32_t jpad;             // row stride in floats
+  uint32_t l2_hints;         // 1: evict_last / evict_first policies; 0: evict_normal
+  double* ylt;               // this layer's YLT row (num_trials doubles)
+  unsigned* err;             // bit0: id out of range, bit1: bad offsets
+  double r2, l2, r3, l3;     // FT2, FT3
+  double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
+};
+
+__device__ __forceinline__ uint64_t make_policy(bool evict_last, bool enabled) {
+  uint64_t p;
+  if (!enabled) {
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  } else if (evict_last) {
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  } else {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  }
+  return p;
+}
+
+__device__ __forceinline__ uint32_t ld_id(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+// Gather V consecutive fp32 of a table row (one vector, V*4 bytes, naturally aligned).
+template <int V>
+__device__ __forceinline__ void ld_row(const float* p, uint64_t pol, float (&x)[V]) {
+  if constexpr (V == 8) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7])
+                 : "l"(p), "l"(pol));
+  } else if constexpr (V == 4) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+                 : "l"(p), "l"(pol));
+  } else if constexpr (V == 2) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                 : "=f"(x[0]), "=f"(x[1])
+                 : "l"(p), "l"(pol));
+  } else {
+    static_assert(V == 1, "V must be 1, 2, 4 or 8");
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(x[0]) : "l"(p), "l"(pol));
+  }
+}
+
+// min(max(x - R, 0), L) in fp64.  Never produces -0.0.
+__device__ __forceinline__ double clamp_terms(double x, double R, double L) {
+  double y = x - R;
+  y = (y > 0.0) ? y : 0.0;
+  return (y < L) ? y : L;
+}
+
+// V: floats per vector load; NV: vectors per row (jpad = V*NV); G: lanes per row (power of 2 <= 32);
+// U: rows per row group per iteration.
+template <int V, int NV, int G, int U>
+__global__ void __launch_bounds__(256) ara_layer_kernel(const __grid_constant__ LayerParams p) {
+  static_assert(32 % G == 0, "G must divide 32");
+  constexpr int RG = 32 / G;              // row groups (rows in flight per warp per u)
+  constexpr int NVL = (NV + G - 1) / G;   // vectors per lane per row
+  constexpr int JP = V * NV;
+  constexpr unsigned FULL = 0xffffffffu;
+
+  __shared__ double s_r1[JP], s_l1[JP];
+  for (int j = threadIdx.x; j < JP; j += blockDim.x) {
+    s_r1[j] = p.r1[j];
+    s_l1[j] = p.l1[j];
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int g = lane % G;
+  const uint64_t pol_tab = make_policy(true, p.l2_hints);
+  const uint64_t pol_yet = make_policy(false, p.l2_hints);
+  const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const double R2 = p.r2, L2 = p.l2;
+
+  for (uint64_t t = warp0; t < p.num_trials; t += nwarps) {
+    uint64_t b, e;
+    unsigned bad = 0;
+    if (p.offsets) {
+      b = p.offsets[t];
+      e = p.offsets[t + 1];
+      if (e < b || e > p.num_events) {  // invalid offsets: flag, contribute nothing
+        bad |= 2u;
+        e = b;
+      }
+    } else {
+      b = t * p.K;
+      e = b + p.K;
+    }
+    double S = 0.0;  // leader's running sum of occurrence-net losses (step 4)
+    for (uint64_t k0 = b; k0 < e; k0 += (uint64_t)RG * U) {
+      uint32_t id[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t q = k0 + (uint64_t)u * RG + grp;
+        uint32_t v = 0;
+        if (q < e) {
+          v = ld_id(p.ids + q, pol_yet);
+          if (v - 1u >= p.C) {  // id outside [1, C]: record, treat as absent
+            bad |= 1u;
+            v = 0;
+          }
+        }
+        id[u] = v;
+      }
+      float x[U][NVL][V];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float* row = p.table + (uint64_t)id[u] * JP;
+#pragma unroll
+        for (int i = 0; i < NVL; ++i) {
+          const int s = g + i * G;
+          if (id[u] != 0 && (NV % G == 0 || s < NV)) {
+            ld_row<V>(row + s * V, pol_tab, x[u][i]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < V; ++c) x[u][i][c] = 0.0f;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        // Steps 1-2: FT1 on every non-zero loss of the row, summed across ELTs (fp64).
+        uint32_t nz = 0;
+#pragma unroll
+        for (int i = 0; i < NVL; ++i)
+#pragma unroll
+          for (int c = 0; c < V; ++c) nz |= __float_as_uint(x[u][i][c]);
+        double s = 0.0;
+        if (nz) {
+#pragma unroll
+          for (int i = 0; i < NVL; ++i)
+#pragma unroll
+            for (int c = 0; c < V; ++c) {
+              if (__float_as_uint(x[u][i][c]) != 0u) {
+                const int j = (g + i * G) * V + c;
+                s += clamp_terms((double)x[u][i][c], s_r1[j], s_l1[j]);
+              }
+            }
+        }
+        if constexpr (G > 1) {
+          if (__any_sync(FULL, s != 0.0)) {
+#pragma unroll
+            for (int off = G / 2; off > 0; off >>= 1) s += __shfl_xor_sync(FULL, s, off);
+          }
+        }
+        // Step 3: occurrence terms FT2; step 4: accumulate (leader lane of the row group).
+        if (s != 0.0 && g == 0) S += clamp_terms(s, R2, L2);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(FULL, S, off);
+    bad = __reduce_or_sync(FULL, bad);
+    if (lane == 0) {
+      p.ylt[t] = clamp_terms(S, p.r3, p.l3);  // step 4: aggregate terms FT3 on S_n
+      if (bad) atomicOr(p.err, bad);
+    }
+  }
+}
+
+}  // namespace ara

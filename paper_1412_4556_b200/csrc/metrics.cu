@@ -1,0 +1,279 @@
+// metrics.cu -- PML and TVaR of a device YLT (PAPER.md:26, :131 name them; readings c11-c14
+// define them): k = ceil(N / RP); PML = k-th largest YLT value; TVaR = mean of the k largest.
+//
+// Device MSD radix SELECT (no full sort): the YLT doubles are mapped to order-preserving uint64 keys
+// and, for all m return periods at once, 8 passes of 8-bit digits narrow each query's key prefix
+// until it is the exact key of its k-th largest value T.  Then one pass computes, per query, the
+// count c and fp64 sum of values with key > T, and TVaR = (sum + (k - c) * T) / k, which is exact
+// under ties (reading c14).  Every pass is one kernel; its last block (ticket counter) finalises the
+// pass on the device, so there is no host round trip until the 2m results are copied back.
+// Sums are reduced in a fixed order (thread -> warp -> block -> blocks in index order), so results
+// are bitwise reproducible run to run.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <vector>
+
+#include "ara.h"
+#include "common.cuh"
+
+namespace ara {
+
+constexpr int kMaxQ = 16;        // queries per kernel batch
+constexpr int kSelBlock = 256;
+
+struct SelState {
+  uint64_t prefix[kMaxQ];  // known high bits of the k-th largest key (right-aligned)
+  uint64_t rank[kMaxQ];    // remaining 1-based rank from the top among keys sharing the prefix
+  uint64_t k[kMaxQ];
+  unsigned int hist[kMaxQ][256];
+  unsigned int ticket;
+  double sum[kMaxQ];       // filled by the tail pass
+  unsigned long long cnt[kMaxQ];
+};
+
+__device__ __forceinline__ uint64_t to_key(double v) {
+  uint64_t b = (uint64_t)__double_as_longlong(v);
+  if (b == 0x8000000000000000ull) b = 0;              // -0.0 == +0.0
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // order-preserving for all non-NaN doubles
+}
+
+__device__ __forceinline__ double from_key(uint64_t k) {
+  uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// One radix pass: histogram of digit `pass` (bits 63-8*pass .. 56-8*pass) over the keys that match
+// each query's prefix; the last block picks each query's digit.
+__global__ void __launch_bounds__(kSelBlock) select_pass(const double* __restrict__ y, uint64_t n, int m, int pass,
+                                                          SelState* st) {
+  __shared__ unsigned int sh[kMaxQ][256];
+  __shared__ uint64_t spre[kMaxQ];
+  __shared__ bool last;
+  for (int i = threadIdx.x; i < m * 256; i += blockDim.x) sh[i / 256][i % 256] = 0;
+  if (threadIdx.x < m) spre[threadIdx.x] = st->prefix[threadIdx.x];
+  __syncthreads();
+  const int shift = 56 - 8 * pass;
+  const unsigned FULL = 0xffffffffu;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // Iterate in warp-uniform trip counts so __match_any_sync sees the whole warp.
+  const uint64_t base0 = (uint64_t)blockIdx.x * blockDim.x;
+  for (uint64_t base = base0; base < n; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const uint64_t key = valid ? to_key(y[i]) : 0;
+    const unsigned digit = (unsigned)(key >> shift) & 0xffu;
+    const uint64_t hi = pass == 0 ? 0 : (key >> (shift + 8));
+    for (int q = 0; q < m; ++q) {
+      const bool hit = valid && hi == spre[q];
+      if (!__any_sync(FULL, hit)) continue;
+      const unsigned tag = hit ? digit : 0x100u;
+      const unsigned peers = __match_any_sync(FULL, tag);
+      if (hit && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&sh[q][digit], __popc(peers));
+      if (pass == 0) {  // all prefixes are empty: one histogram serves every query
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  const int nq = pass == 0 ? 1 : m;
+  for (int i = threadIdx.x; i < nq * 256; i += blockDim.x) {
+    unsigned v = sh[i / 256][i % 256];
+    if (v) atomicAdd(&st->hist[i / 256][i % 256], v);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(&st->ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < m) {
+    const int q = threadIdx.x;
+    const int hq = pass == 0 ? 0 : q;
+    volatile unsigned int* h = st->hist[hq];
+    uint64_t r = st->rank[q], above = 0;
+    int d = 255;
+    for (; d > 0; --d) {
+      uint64_t c = h[d];
+      if (above + c >= r) break;
+      above += c;
+    }
+    st->rank[q] = r - above;
+    st->prefix[q] = (st->prefix[q] << 8) | (uint64_t)d;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxQ * 256; i += blockDim.x) st->hist[i / 256][i % 256] = 0;
+  if (threadIdx.x == 0) st->ticket = 0;
+}
+
+// Tail pass: per query, count and fp64-sum the values with key > T (T = full prefix after 8 passes).
+// Block partials go to part[block][q]; the last block adds them in block order.
+__global__ void __launch_bounds__(kSelBlock) tail_pass(const double* __restrict__ y, uint64_t n, int m, SelState* st,
+                                                        double* __restrict__ psum,
+                                                        unsigned long long* __restrict__ pcnt, double* __restrict__ out) {
+  __shared__ uint64_t sT[kMaxQ];
+  __shared__ double wsum[kSelBlock / 32][kMaxQ];
+  __shared__ unsigned long long wcnt[kSelBlock / 32][kMaxQ];
+  __shared__ bool last;
+  if (threadIdx.x < m) sT[threadIdx.x] = st->prefix[threadIdx.x];
+  __syncthreads();
+  double s[kMaxQ];
+  unsigned long long c[kMaxQ];
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) {
+    s[q] = 0.0;
+    c[q] = 0;
+  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = y[i];
+    const uint64_t key = to_key(v);
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q) {
+      if (q < m && key > sT[q]) {
+        s[q] += v;
+        c[q] += 1;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) {
+    if (q >= m) break;
+    double a = s[q];
+    unsigned long long b = c[q];
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+      b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    if (lane == 0) {
+      wsum[w][q] = a;
+      wcnt[w][q] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < m) {
+    double a = 0.0;
+    unsigned long long b = 0;
+    for (int i = 0; i < kSelBlock / 32; ++i) {
+      a += wsum[i][threadIdx.x];
+      b += wcnt[i][threadIdx.x];
+    }
+    psum[(uint64_t)blockIdx.x * kMaxQ + threadIdx.x] = a;
+    pcnt[(uint64_t)blockIdx.x * kMaxQ + threadIdx.x] = b;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(&st->ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < m) {
+    const int q = threadIdx.x;
+    double a = 0.0;
+    unsigned long long b = 0;
+    for (unsigned i = 0; i < gridDim.x; ++i) {
+      a += ((volatile double*)psum)[(uint64_t)i * kMaxQ + q];
+      b += ((volatile unsigned long long*)pcnt)[(uint64_t)i * kMaxQ + q];
+    }
+    const double T = from_key(sT[q]);
+    const uint64_t k = st->k[q];
+    out[q] = T;                                            // PML: the k-th largest value
+    out[kMaxQ + q] = __ddiv_rn(__dadd_rn(a, __dmul_rn((double)(k - b), T)), (double)k);  // TVaR (no FMA contraction)
+  }
+  if (threadIdx.x == 0) st->ticket = 0;
+}
+
+// k = ceil(n / RP) (reading c12): exact integer ceil for integral RP, fuzzed otherwise.  0 = invalid.
+static uint64_t metric_rank(uint64_t n, double rp) {
+  if (!(rp > 1.0) || !(rp <= (double)n) || !isfinite(rp)) return 0;
+  if (rp == floor(rp) && rp < 9007199254740992.0) {
+    const uint64_t r = (uint64_t)rp;
+    return n / r + (n % r ? 1 : 0);
+  }
+  const double x = (double)n / rp;
+  return (uint64_t)ceil(x - 1e-9 * x);
+}
+
+static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml, double* tvar,
+                          cudaStream_t s) {
+  if (!ylt || !rps || n == 0 || m == 0 || m > ARA_MAX_RETURN_PERIODS)
+    return set_error(ARA_E_ARG, "invalid metric arguments");
+  std::vector<uint64_t> ks(m);
+  for (uint32_t i = 0; i < m; ++i) {
+    ks[i] = metric_rank(n, rps[i]);
+    if (!ks[i]) return set_error(ARA_E_RANGE, "return period %g outside (1, %llu]", rps[i], (unsigned long long)n);
+  }
+  int dev = 0, sms = 148;
+  ARA_CUDA(cudaGetDevice(&dev));
+  ARA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  uint64_t blocks = (n + kSelBlock - 1) / kSelBlock;
+  if (blocks > (uint64_t)sms * 4) blocks = (uint64_t)sms * 4;
+  SelState* st = nullptr;
+  double* psum = nullptr;
+  unsigned long long* pcnt = nullptr;
+  double* d_out = nullptr;
+  const size_t bytes = sizeof(SelState) + blocks * kMaxQ * (sizeof(double) + sizeof(unsigned long long)) +
+                       2 * kMaxQ * sizeof(double);
+  char* scratch = nullptr;
+  ARA_CUDA(cudaMallocAsync((void**)&scratch, bytes, s));
+  st = (SelState*)scratch;
+  psum = (double*)(scratch + sizeof(SelState));
+  pcnt = (unsigned long long*)(psum + blocks * kMaxQ);
+  d_out = (double*)(pcnt + blocks * kMaxQ);
+  std::vector<double> h_out(2 * kMaxQ);
+  SelState init;
+  ara_status rc = ARA_OK;
+  for (uint32_t q0 = 0; q0 < m && rc == ARA_OK; q0 += kMaxQ) {
+    const int mq = (int)std::min<uint32_t>(kMaxQ, m - q0);
+    memset(&init, 0, sizeof init);
+    for (int q = 0; q < mq; ++q) {
+      init.rank[q] = ks[q0 + q];
+      init.k[q] = ks[q0 + q];
+    }
+    cudaError_t e = cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s);
+    for (int pass = 0; pass < 8 && e == cudaSuccess; ++pass) {
+      select_pass<<<(unsigned)blocks, kSelBlock, 0, s>>>(ylt, n, mq, pass, st);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      tail_pass<<<(unsigned)blocks, kSelBlock, 0, s>>>(ylt, n, mq, st, psum, pcnt, d_out);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.data(), d_out, 2 * kMaxQ * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      rc = cuda_error(e, "metric kernels");
+      break;
+    }
+    for (int q = 0; q < mq; ++q) {
+      if (pml) pml[q0 + q] = h_out[q];
+      if (tvar) tvar[q0 + q] = h_out[kMaxQ + q];
+    }
+  }
+  cudaFreeAsync(scratch, s);
+  return rc;
+}
+
+}  // namespace ara
+
+extern "C" {
+
+ara_status ara_pml_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_out,
+                        double* tvar_out, void* stream) {
+  if (!pml_out && !tvar_out) return ara::set_error(ARA_E_ARG, "no output");
+  return ara::metrics(ylt, n, rps, m, pml_out, tvar_out, (cudaStream_t)stream);
+}
+
+ara_status ara_pml(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream) {
+  if (!out) return ara::set_error(ARA_E_ARG, "out is NULL");
+  return ara::metrics(ylt, n, rps, m, out, nullptr, (cudaStream_t)stream);
+}
+
+ara_status ara_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream) {
+  if (!out) return ara::set_error(ARA_E_ARG, "out is NULL");
+  return ara::metrics(ylt, n, rps, m, nullptr, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

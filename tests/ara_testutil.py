@@ -24,3 +24,55 @@ def golden_layer(d):
     return (l["elts"], (l["ft2"][0], inf_or(l["ft2"][1])), (l["ft3"][0], inf_or(l["ft3"][1])))
 
 
+
+
+# ---------------------------------------------------------------- GPU-path helpers (tests only)
+def gpu_ylt(cfg_or_none, ctx, event_ids_np, offsets_np=None, K=0, num_trials=None, num_layers=1, variant=None,
+            block_threads=None, check=True):
+    """Copy a host YET to the device, run ara_run, return the YLT [layers, trials] as numpy."""
+    import numpy as np
+    import torch
+    from paper_1412_4556_b200 import ara
+    dev = torch.device("cuda:0")
+    ids = torch.from_numpy(np.ascontiguousarray(event_ids_np, dtype=np.uint32).view(np.int32)).to(dev)
+    off = None
+    if offsets_np is not None:
+        off = torch.from_numpy(np.ascontiguousarray(offsets_np, dtype=np.uint64).view(np.int64)).to(dev)
+        n = len(offsets_np) - 1
+    else:
+        n = num_trials if num_trials is not None else (ids.numel() // K if K else 0)
+    ylt = torch.full((num_layers, max(n, 1)), -7.0, dtype=torch.float64, device=dev)
+    if variant is not None:
+        ctx.ara_set_option(ara.ARA_OPT_VARIANT, variant)
+    if block_threads is not None:
+        ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, block_threads)
+    ctx.ara_run(ids, ylt, offsets=off, events_per_trial=K, num_trials=n)
+    if check:
+        ctx.ara_check()
+    torch.cuda.synchronize()
+    return ylt[:, :n].cpu().numpy()
+
+
+def golden_context(d, layers_override=None):
+    import numpy as np
+    from paper_1412_4556_b200 import ara
+    elts = [ara.Elt(np.array(e["ids"], np.uint32), np.array(e["losses"], np.float32), e["ft1"][0], inf_or(e["ft1"][1]))
+            for e in d["elts"]]
+    l = d["layer"]
+    layers = layers_override or [ara.Layer(l["elts"], l["ft2"][0], inf_or(l["ft2"][1]), l["ft3"][0], inf_or(l["ft3"][1]))]
+    return ara.Context(d["catalog_size"], elts, layers, device=0)
+
+
+def ragged(trials):
+    import numpy as np
+    ids = np.array([e for t in trials for e in t], dtype=np.uint32)
+    off = np.zeros(len(trials) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(t) for t in trials])
+    return ids, off
+
+
+def within_tol(gpu, ref, rel=1e-6, abs_floor=1e-3):
+    """north_star parity: |gpu - oracle| <= max(1e-6 |oracle|, 1e-3)."""
+    import numpy as np
+    gpu, ref = np.asarray(gpu), np.asarray(ref)
+    return np.abs(gpu - ref) <= np.maximum(rel * np.abs(ref), abs_floor)

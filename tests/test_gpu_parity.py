@@ -1,0 +1,299 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerance (north_star): |gpu - oracle| <= max(1e-6 |oracle|, 1e-3) for the real regime; BITWISE in
+the integer regime, where every fp64 operation of both paths is exact, and for
+the hand-worked golden values.  Inputs come from the shared generator (synth) or the golden files;
+no oracle input or expected value is ever produced by the CUDA path.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from ara_testutil import gpu_ylt, golden, golden_context, golden_elts, golden_layer, ragged, within_tol
+from paper_1412_4556_b200 import ara, synth
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+
+def _oracle_cfg(cfg, elts, yet):
+    return oracle.ylt_for(cfg, elts, yet)
+
+
+# ------------------------------------------------------------------ generator
+def test_device_generator_matches_host(cuda_device):
+    for C, q0, n in [(10_000, 0, 100_003), (2_000_000, 123_456_789, 65_536), (10_000_000, 7_999_999_000, 4099),
+                     (1, 0, 17), (2**32 - 1, 2**40, 1000)]:
+        out = torch.empty(n, dtype=torch.int32, device=cuda_device)
+        synth.yet_ids_device(out.data_ptr(), synth.SEED, C, q0, n, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, synth.yet_ids(synth.SEED, C, q0, n)), (C, q0, n)
+
+
+# ------------------------------------------------------------------ table build (A0)
+def test_table_rows_exhaustive_tiny(cuda_device):
+    cfg = synth.Config.load("T")
+    elts = synth.make_elts(cfg)
+    ctx = ara.context_for_config(cfg, elts)
+    info = ctx.ara_layer_info(0)
+    assert info["table_bytes"] == 80008 and info["row_stride"] == 8
+    want = np.zeros((cfg.catalog_size + 1, 2), np.float32)
+    for m, j in enumerate(cfg.layers[0].elts):
+        want[elts[j].event_ids, m] = elts[j].losses
+    for e in range(cfg.catalog_size + 1):
+        assert np.array_equal(ctx.ara_table_row(0, e), want[e]), e
+    assert np.count_nonzero(want == 0) == 2 * (cfg.catalog_size + 1) - 2 * cfg.entries_per_elt
+
+
+# ------------------------------------------------------------------ golden worked examples (bitwise)
+def test_spec_worked_trial_gpu(cuda_device):
+    g = golden("spec_trial_example.json")
+    ctx = golden_context(g)
+    y = gpu_ylt(None, ctx, np.array(g["trial"]), K=len(g["trial"]), num_trials=1)
+    assert y[0, 0] == 140.0
+
+
+def test_extended_example_gpu(cuda_device):
+    g = golden("extended_example.json")
+    ctx = golden_context(g)
+    ids, off = ragged(g["trials"])
+    y = gpu_ylt(None, ctx, ids, offsets_np=off)
+    assert list(y[0]) == g["ylt"]
+    ctx2 = golden_context(g, layers_override=[ara.Layer(g["layer"]["elts"])])
+    elts_id = [ara.Elt(np.array(e["ids"], np.uint32), np.array(e["losses"], np.float32)) for e in g["elts"]]
+    ctx2 = ara.Context(g["catalog_size"], elts_id, [ara.Layer(g["layer"]["elts"])])
+    y2 = gpu_ylt(None, ctx2, np.array(g["identity_terms"]["trial"]), K=5, num_trials=1)
+    assert y2[0, 0] == 2380.0
+
+
+def test_brute_force_short_trials_gpu(cuda_device):
+    import itertools
+    g = golden("extended_example.json")
+    trials = [list(t) for n in range(4) for t in itertools.product([1, 2, 3, 4], repeat=n)]
+    ids, off = ragged(trials)
+    want = oracle.ylt(g["catalog_size"], ids, off, len(trials), 0, golden_elts(g), [golden_layer(g)])
+    y = gpu_ylt(None, golden_context(g), ids, offsets_np=off)
+    assert np.array_equal(y, want)
+
+
+# ------------------------------------------------------------------ configs
+def test_tiny_config_bitwise_all_variants_and_shapes(cuda_device):
+    cfg = synth.Config.load("T")
+    elts = synth.make_elts(cfg)
+    yet = synth.make_yet(cfg)
+    want = _oracle_cfg(cfg, elts, yet)
+    ctx = ara.context_for_config(cfg, elts)
+    nvar = ctx.ara_layer_info(0)["num_variants"]
+    for v in range(nvar):
+        for bt in (64, 256):
+            y = gpu_ylt(cfg, ctx, yet.event_ids, K=cfg.kmin, variant=v, block_threads=bt)
+            assert np.array_equal(y, want), (v, bt)
+    assert not np.any(np.signbit(y))
+
+
+def test_variable_length_config_within_tolerance(cuda_device):
+    cfg = synth.Config.load("V")
+    elts = synth.make_elts(cfg)
+    yet = synth.make_yet(cfg)
+    want = _oracle_cfg(cfg, elts, yet)
+    ctx = ara.context_for_config(cfg, elts)
+    y = gpu_ylt(cfg, ctx, yet.event_ids, offsets_np=yet.offsets)
+    assert np.all(within_tol(y, want))
+    assert np.max(np.abs(y - want) / np.maximum(np.abs(want), 1.0)) < 1e-12  # in practice far inside 1e-6
+    # metrics of each path's own YLT
+    rps = synth.return_periods(cfg.num_trials)
+    p, t = ara.ara_pml_tvar(torch.from_numpy(y[0]).cuda(), rps)
+    assert np.all(within_tol(p, oracle.pml(want[0], rps))) and np.all(within_tol(t, oracle.tvar(want[0], rps)))
+
+
+def _small_problem(J, C=5000, n=300, K=37, N=333, integer=True, seed=0, inf_limits=False, zero_ret=False,
+                   empty_elts=()):
+    rng = np.random.default_rng(seed + 1000 * J)
+    elts = []
+    for j in range(J):
+        cnt = 0 if j in empty_elts else n
+        ids = rng.choice(np.arange(1, C + 1), size=cnt, replace=False).astype(np.uint32)
+        losses = (rng.integers(1, 1 << 20, size=cnt) if integer else rng.random(cnt) * 1e6 + 0.5).astype(np.float32)
+        r = 0.0 if zero_ret else float(rng.integers(0, 1 << 18))
+        l = INF if (inf_limits or j % 3 == 1) else float(rng.integers(1 << 18, 1 << 21))
+        elts.append((ids, losses, (r, l)))
+    # ids 1 and C present
+    yet = rng.integers(1, C + 1, size=N * K).astype(np.uint32)
+    yet[0], yet[-1] = 1, C
+    layer = (list(range(J)), (0.0 if zero_ret else 5000.0, INF if inf_limits else float(1 << 22)),
+             (0.0 if zero_ret else 2e5, INF if inf_limits else 4e6))
+    return C, elts, layer, yet, N, K
+
+
+def _ctx_from(C, elts, layers):
+    return ara.Context(C, [ara.Elt(i, l, r, lim) for i, l, (r, lim) in elts],
+                       [ara.Layer(idx, a[0], a[1], b[0], b[1]) for idx, a, b in layers])
+
+
+@pytest.mark.parametrize("J", [1, 2, 3, 4, 5, 8, 9, 15, 16, 17, 24, 31, 33, 64, 100, 128])
+def test_every_row_width_bitwise(cuda_device, J):
+    C, elts, layer, yet, N, K = _small_problem(J)
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx_from(C, elts, [layer])
+    for v in range(ctx.ara_layer_info(0)["num_variants"]):
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, variant=v), want), v
+
+
+@pytest.mark.parametrize("kw", [dict(inf_limits=True), dict(zero_ret=True), dict(zero_ret=True, inf_limits=True),
+                                dict(empty_elts=(0, 2)), dict(integer=False)])
+def test_term_edge_cases(cuda_device, kw):
+    C, elts, layer, yet, N, K = _small_problem(16, **kw)
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    y = gpu_ylt(None, _ctx_from(C, elts, [layer]), yet, K=K)
+    if kw.get("integer", True):
+        assert np.array_equal(y, want)
+    else:
+        assert np.all(within_tol(y, want))
+
+
+def test_ragged_trial_lengths(cuda_device):
+    lens = [0, 1, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 1000, 1500, 0, 2]
+    C, elts, layer, _, _, _ = _small_problem(16)
+    rng = np.random.default_rng(5)
+    trials = [list(rng.integers(1, C + 1, size=k)) for k in lens]
+    ids, off = ragged(trials)
+    want = oracle.ylt(C, ids, off, len(trials), 0, elts, [layer])
+    ctx = _ctx_from(C, elts, [layer])
+    for v in range(ctx.ara_layer_info(0)["num_variants"]):
+        assert np.array_equal(gpu_ylt(None, ctx, ids, offsets_np=off, variant=v), want)
+    # offsets that do not start at 0 (a shard of a bigger YET): prefix junk ids must be ignored
+    off2 = off + np.uint64(3)
+    ids2 = np.concatenate([np.array([C + 5, 0, 9], np.uint32), ids])
+    assert np.array_equal(gpu_ylt(None, ctx, ids2, offsets_np=off2), want)
+
+
+def test_multi_layer_distinct_widths(cuda_device):
+    C, elts, layer, yet, N, K = _small_problem(24, seed=3)
+    layers = [layer, ([5, 1, 7], (100.0, 1e6), (0.0, INF)), (list(range(17)), (0.0, INF), (1e5, 2e6)),
+              ([23], (0.0, INF), (0.0, INF))]
+    want = oracle.ylt(C, yet, None, N, K, elts, layers)
+    y = gpu_ylt(None, _ctx_from(C, elts, layers), yet, K=K, num_layers=len(layers))
+    assert np.array_equal(y, want)
+
+
+def test_invalid_ids_reported(cuda_device):
+    C, elts, layer, yet, N, K = _small_problem(4)
+    ctx = _ctx_from(C, elts, [layer])
+    for bad in (0, C + 1, 2**32 - 1):
+        y = yet.copy()
+        y[17] = bad
+        with pytest.raises(ara.AraError) as ei:
+            gpu_ylt(None, ctx, y, K=K)
+        assert ei.value.status == ara.ARA_E_RANGE
+    gpu_ylt(None, ctx, yet, K=K)  # flag was cleared
+
+
+def test_bad_offsets_reported(cuda_device):
+    C, elts, layer, yet, N, K = _small_problem(4)
+    ctx = _ctx_from(C, elts, [layer])
+    off = np.array([0, 10, 5, 20], np.uint64)
+    with pytest.raises(ara.AraError) as ei:
+        gpu_ylt(None, ctx, yet[:20], offsets_np=off)
+    assert ei.value.status == ara.ARA_E_ARG
+    off = np.array([0, 10, 30], np.uint64)
+    with pytest.raises(ara.AraError):
+        gpu_ylt(None, ctx, yet[:20], offsets_np=off)
+
+
+def test_determinism_and_launch_shape_invariance_real_regime(cuda_device):
+    C, elts, layer, yet, N, K = _small_problem(16, integer=False, N=2000, K=200)
+    ctx = _ctx_from(C, elts, [layer])
+    base = gpu_ylt(None, ctx, yet, K=K)
+    for _ in range(3):
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K), base)
+    for bps in (1, 2, 7):
+        ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, bps)
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K), base)
+    ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, 0)
+    for pol in (1, 2, 0):
+        ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, pol)
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K), base)
+    assert np.all(within_tol(base, oracle.ylt(C, yet, None, N, K, elts, [layer])))
+
+
+# ------------------------------------------------------------------ end-to-end host path
+def test_run_host_matches_device_path(cuda_device):
+    for name in ("T", "V"):
+        cfg = synth.Config.load(name)
+        elts = synth.make_elts(cfg)
+        yet = synth.make_yet(cfg)
+        ctx = ara.context_for_config(cfg, elts)
+        dev = gpu_ylt(cfg, ctx, yet.event_ids, offsets_np=yet.offsets, K=yet.events_per_trial,
+                      num_trials=yet.num_trials)
+        ids = torch.from_numpy(yet.event_ids.view(np.int32)).pin_memory()
+        out = torch.zeros((1, yet.num_trials), dtype=torch.float64).pin_memory()
+        ctx.ara_run_host(ids, out, offsets=yet.offsets, events_per_trial=yet.events_per_trial,
+                         num_trials=yet.num_trials)
+        assert np.array_equal(out.numpy(), dev)
+        pageable = np.zeros((1, yet.num_trials))
+        ctx.ara_run_host(yet.event_ids, pageable, offsets=yet.offsets, events_per_trial=yet.events_per_trial,
+                         num_trials=yet.num_trials)
+        assert np.array_equal(pageable, dev)
+
+
+# ------------------------------------------------------------------ metrics kernels
+@pytest.mark.parametrize("case", ["ties", "uniform", "small", "negzero", "many_rps", "one"])
+def test_metrics_match_oracle(cuda_device, case):
+    rng = np.random.default_rng(11)
+    rps = [2.0, 5.0, 10.0, 20.0, 25.0, 50.0, 100.0, 200.0, 250.0, 500.0, 1000.0]
+    if case == "ties":
+        y = np.floor(rng.exponential(1000.0, 100_000)) * (rng.random(100_000) > 0.3)
+        y[rng.random(100_000) < 0.2] = 4000.0
+    elif case == "uniform":
+        y = rng.random(1_000_003) * 1e9
+    elif case == "small":
+        y = np.array([3.0, 1.0, 2.0])
+        rps = [1.5, 2.0, 3.0]
+    elif case == "negzero":
+        y = np.array([0.0, -0.0, 5.0, -0.0, 1.0, 0.0])
+        rps = [2.0, 6.0, 1.2]
+    elif case == "many_rps":
+        y = rng.random(50_000) * 100
+        rps = list(np.linspace(1.01, 50_000, 70)) + [8 / 3, 7.0 / 3]
+    else:
+        y = np.array([42.0])
+        rps = []
+    if not rps:
+        with pytest.raises(ara.AraError):
+            ara.ara_pml_tvar(torch.from_numpy(y).cuda(), rps)
+        return
+    d = torch.from_numpy(y).cuda()
+    p, t = ara.ara_pml_tvar(d, rps)
+    assert np.array_equal(p, oracle.pml(y, rps))
+    assert np.all(within_tol(t, oracle.tvar(y, rps), rel=1e-12, abs_floor=1e-9))
+    if case in ("ties", "small", "negzero"):  # integer-valued: exact
+        assert np.array_equal(t, oracle.tvar(y, rps))
+    assert np.array_equal(ara.ara_pml(d, rps), p) and np.array_equal(ara.ara_tvar(d, rps), t)
+    p2, t2 = ara.ara_pml_tvar(d, rps)
+    assert np.array_equal(p2, p) and np.array_equal(t2, t)  # deterministic
+
+
+# ------------------------------------------------------------------ fake multi-GPU (shards on one GPU)
+def test_sharded_runs_reassemble_bitwise(cuda_device):
+    from paper_1412_4556_b200 import dist
+    cfg = synth.Config.load("V")
+    elts = synth.make_elts(cfg)
+    full = synth.make_yet(cfg)
+    ctx = ara.context_for_config(cfg, elts)
+    want = gpu_ylt(cfg, ctx, full.event_ids, offsets_np=full.offsets)
+    for G in (2, 3, 8):
+        starts = dist.shard_starts(cfg.num_trials, G)
+        cap = dist.shard_cap(cfg.num_trials, G)
+        gathered = torch.full((G, 1, cap), -1.0, dtype=torch.float64, device=cuda_device)
+        for g in range(G):
+            y = synth.make_yet(cfg, starts[g], starts[g + 1])
+            gathered[g, :, :starts[g + 1] - starts[g]] = torch.from_numpy(
+                gpu_ylt(cfg, ctx, y.event_ids, offsets_np=y.offsets)).cuda()
+        out = torch.empty((1, cfg.num_trials), dtype=torch.float64, device=cuda_device)
+        ara.ara_unshard(gathered, G, cap, 1, starts, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), want), G
