@@ -158,12 +158,20 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *   ARA_OPT_BLOCKS_PER_SM   resident blocks per SM the persistent grid is sized for
  *   ARA_OPT_L2_POLICY       0 default (evict_last hints on table rows, evict_first on YET ids),
  *                           1 no hints, 2 hints + persisting access-policy window on the table
- *   ARA_OPT_VARIANT         kernel variant index within the J class (ara_variant_count) */
+ *   ARA_OPT_VARIANT         kernel variant index within the selected kernel and row width
+ *                           (ara_layer_info reports the count)
+ *   ARA_OPT_KERNEL          0 presence (default): a per-layer presence bitmap of the table's non-zero
+ *                           rows, staged in shared memory, so only rows that hold a loss are gathered;
+ *                           1 dense: every occurrence gathers its full row.  Identical results (an
+ *                           all-zero row contributes exactly 0, reading c9).
+ *                           Selecting a kernel resets ARA_OPT_VARIANT to 0.
+ * ARA_OPT_BLOCK_THREADS applies to the dense kernel; the presence kernel fixes its block size. */
 typedef enum {
   ARA_OPT_BLOCK_THREADS = 1,
   ARA_OPT_BLOCKS_PER_SM = 2,
   ARA_OPT_L2_POLICY = 3,
-  ARA_OPT_VARIANT = 4
+  ARA_OPT_VARIANT = 4,
+  ARA_OPT_KERNEL = 5
 } ara_option;
 ARA_API ara_status ara_set_option(ara_ctx* ctx, ara_option opt, int64_t value);
 ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);

@@ -4,6 +4,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -13,6 +14,8 @@
 
 #include "ara.h"
 #include "ara_kernel.cuh"
+#include "presence_kernel.cuh"
+#include "variants.cuh"
 #include "common.cuh"
 
 namespace ara {
@@ -43,47 +46,12 @@ static uint32_t row_floats(uint32_t J) {
 }
 
 // ------------------------------------------------------------------------------------------ variants
-typedef void (*KernelFn)(LayerParams);
-
-struct Variant {
-  uint32_t jpad;
-  int V, NV, G, U;
-  KernelFn fn;
-  const char* name;
-};
-
-#define ARA_VAR(V_, NV_, G_, U_) \
-  {(uint32_t)((V_) * (NV_)), V_, NV_, G_, U_, ara_layer_kernel<V_, NV_, G_, U_>, \
-   "ara_layer_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",U=" #U_ ">"}
-
-// First entry per jpad is the default (chosen from the launch-shape sweep).
-static const Variant kVariants[] = {
-    ARA_VAR(1, 1, 1, 8),  ARA_VAR(1, 1, 1, 16),
-    ARA_VAR(2, 1, 1, 8),  ARA_VAR(2, 1, 1, 16),
-    ARA_VAR(4, 1, 1, 8),  ARA_VAR(4, 1, 1, 16),
-    ARA_VAR(8, 1, 1, 8),  ARA_VAR(8, 1, 1, 4),
-    ARA_VAR(8, 2, 2, 8),  ARA_VAR(8, 2, 2, 4),  ARA_VAR(8, 2, 1, 4), ARA_VAR(8, 2, 2, 16), ARA_VAR(8, 2, 1, 8),
-    ARA_VAR(8, 3, 4, 8),  ARA_VAR(8, 3, 2, 4),
-    ARA_VAR(8, 4, 4, 8),  ARA_VAR(8, 4, 2, 4),
-    ARA_VAR(8, 5, 8, 8),  ARA_VAR(8, 5, 4, 4),
-    ARA_VAR(8, 6, 8, 8),  ARA_VAR(8, 6, 4, 4),
-    ARA_VAR(8, 7, 8, 8),  ARA_VAR(8, 7, 4, 4),
-    ARA_VAR(8, 8, 8, 8),  ARA_VAR(8, 8, 4, 4),
-    ARA_VAR(8, 9, 8, 4),  ARA_VAR(8, 9, 16, 8),
-    ARA_VAR(8, 10, 8, 4), ARA_VAR(8, 10, 16, 8),
-    ARA_VAR(8, 11, 8, 4), ARA_VAR(8, 11, 16, 8),
-    ARA_VAR(8, 12, 8, 4), ARA_VAR(8, 12, 16, 8),
-    ARA_VAR(8, 13, 8, 4), ARA_VAR(8, 13, 16, 8),
-    ARA_VAR(8, 14, 8, 4), ARA_VAR(8, 14, 16, 8),
-    ARA_VAR(8, 15, 8, 4), ARA_VAR(8, 15, 16, 8),
-    ARA_VAR(8, 16, 8, 4), ARA_VAR(8, 16, 16, 8),
-};
-static const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
-
-static void variants_for(uint32_t jpad, std::vector<const Variant*>& out) {
+static void variants_for(int kind, uint32_t jpad, std::vector<const Variant*>& out) {
   out.clear();
-  for (int i = 0; i < kNumVariants; ++i)
-    if (kVariants[i].jpad == jpad) out.push_back(&kVariants[i]);
+  int n = 0;
+  const Variant* t = kind == KIND_PRESENCE ? presence_variants(&n) : dense_variants(&n);
+  for (int i = 0; i < n; ++i)
+    if (t[i].jpad == jpad) out.push_back(&t[i]);
 }
 
 // ------------------------------------------------------------------------------------------ context
@@ -91,7 +59,9 @@ struct Layer {
   uint32_t J = 0, jpad = 0;
   float* table = nullptr;
   uint64_t table_bytes = 0;
-  std::vector<const Variant*> variants;
+  uint32_t* present = nullptr;  // presence bitmap, (C + 1 + 31) / 32 words
+  uint32_t present_words = 0;
+  std::vector<const Variant*> variants[2];  // by KernelKind
   double r1[kMaxJ], l1[kMaxJ];
   double r2 = 0, l2 = 0, r3 = 0, l3 = 0;
 };
@@ -110,7 +80,9 @@ struct ara_ctx {
   int blocks_per_sm = 0;
   int l2_policy = 0;
   int variant = 0;
+  int kernel = 0;  // KernelKind
   int persist_max = 0, window_max = 0;
+  int smem_optin = 0;
   // end-to-end host path
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
@@ -182,11 +154,24 @@ __global__ void __launch_bounds__(256) scatter_kernel(float* __restrict__ table,
     table[(uint64_t)ids[i] * jpad + col[i]] = losses[i];
 }
 
+// Build the presence bitmap of one layer: bit id of present[] for every ELT entry of the layer.
+__global__ void __launch_bounds__(256) presence_build_kernel(uint32_t* __restrict__ present,
+                                                             const uint32_t* __restrict__ ids, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = ids[i];
+    atomicOr(present + (id >> 5), 1u << (id & 31u));
+  }
+}
+
+
 static void destroy_ctx(ara_ctx* c) {
   if (!c) return;
   DeviceGuard guard(c->device);
   cudaDeviceSynchronize();
-  for (auto& L : c->layers) cudaFree(L.table);
+  for (auto& L : c->layers) {
+    cudaFree(L.table);
+    cudaFree(L.present);
+  }
   cudaFree(c->d_err);
   cudaFreeHost(c->h_err);
   for (int i = 0; i < 2; ++i) {
@@ -202,9 +187,10 @@ static void destroy_ctx(ara_ctx* c) {
 }
 
 static const Variant* pick(const ara_ctx* c, const Layer& L) {
+  const auto& vs = L.variants[c->kernel];
   int v = c->variant;
-  if (v < 0 || v >= (int)L.variants.size()) v = 0;
-  return L.variants[v];
+  if (v < 0 || v >= (int)vs.size()) v = 0;
+  return vs[v];
 }
 
 static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, const uint64_t* offsets,
@@ -233,12 +219,26 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
     p.r1[j] = L.r1[j];
     p.l1[j] = L.l1[j];
   }
+  int threads = c->block_threads;
+  size_t dyn_smem = 0;
+  if (var->kind == KIND_PRESENCE) {
+    threads = var->NW * 32;
+    cudaFuncAttributes fa;
+    ARA_CUDA(cudaFuncGetAttributes(&fa, (const void*)var->fn));
+    const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)var->NW * kQueue * 4;
+    if (budget < 4096) return set_error(ARA_E_UNSUPPORTED, "no shared memory left for the presence bitmap");
+    p.present = L.present;
+    p.present_words = L.present_words;
+    p.fold_words = (uint32_t)std::min<int64_t>(L.present_words, budget / 4);
+    dyn_smem = ((size_t)p.fold_words + (size_t)var->NW * kQueue) * 4;
+    ARA_CUDA(cudaFuncSetAttribute((const void*)var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
+  }
   int bps = c->blocks_per_sm;
   if (bps <= 0) {
-    ARA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)var->fn, c->block_threads, 0));
+    ARA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)var->fn, threads, dyn_smem));
     if (bps < 1) bps = 1;
   }
-  uint64_t warps_per_block = c->block_threads / 32;
+  uint64_t warps_per_block = threads / 32;
   uint64_t blocks = (uint64_t)c->sms * bps;
   uint64_t need = (num_trials + warps_per_block - 1) / warps_per_block;
   if (blocks > need) blocks = need;
@@ -246,7 +246,8 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3((unsigned)blocks);
-  cfg.blockDim = dim3(c->block_threads);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = dyn_smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   if (c->l2_policy == 2 && c->window_max > 0) {
@@ -333,6 +334,7 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
   c->C = catalog_size;
   cudaDeviceGetAttribute(&c->persist_max, cudaDevAttrMaxPersistingL2CacheSize, device);
   cudaDeviceGetAttribute(&c->window_max, cudaDevAttrMaxAccessPolicyWindowSize, device);
+  cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
 
 #define FAIL(x)          \
   do {                   \
@@ -361,8 +363,10 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
     const ara_layer& in = layers[l];
     L.J = in.num_elts;
     L.jpad = row_floats(L.J);
-    variants_for(L.jpad, L.variants);
-    if (L.variants.empty()) FAIL(set_error(ARA_E_UNSUPPORTED, "no kernel for row width %u", L.jpad));
+    variants_for(KIND_PRESENCE, L.jpad, L.variants[KIND_PRESENCE]);
+    variants_for(KIND_DENSE, L.jpad, L.variants[KIND_DENSE]);
+    if (L.variants[0].empty() || L.variants[1].empty())
+      FAIL(set_error(ARA_E_UNSUPPORTED, "no kernel for row width %u", L.jpad));
     for (int j = 0; j < kMaxJ; ++j) {
       L.r1[j] = 0.0;
       L.l1[j] = INFINITY;
@@ -381,6 +385,12 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       FAIL(set_error(ARA_E_NOMEM, "table of %llu bytes for layer %u", (unsigned long long)L.table_bytes, l));
     }
     CK(cudaMemsetAsync(L.table, 0, L.table_bytes, s));
+    L.present_words = (uint32_t)(((uint64_t)catalog_size + 1 + 31) / 32);
+    if (cudaMalloc(&L.present, (size_t)L.present_words * 4) != cudaSuccess) {
+      cudaGetLastError();
+      FAIL(set_error(ARA_E_NOMEM, "presence bitmap for layer %u", l));
+    }
+    CK(cudaMemsetAsync(L.present, 0, (size_t)L.present_words * 4, s));
     h_ids.clear();
     h_col.clear();
     h_loss.clear();
@@ -400,6 +410,8 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       CK(cudaMemcpyAsync(d_loss, h_loss.data(), n * 4, cudaMemcpyHostToDevice, s));
       uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)c->sms * 8);
       scatter_kernel<<<(unsigned)blocks, 256, 0, s>>>(L.table, L.jpad, d_ids, d_loss, d_col, n);
+      CK(cudaGetLastError());
+      presence_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(L.present, d_ids, n);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(s));  // host staging vectors are reused for the next layer
       cudaFree(d_ids);
@@ -483,6 +495,13 @@ ara_status ara_run_host(ara_ctx* c, const ara_yet* yet, double* ylt_host, void* 
     c->st_cap_ids = cap_ids;
     c->st_cap_trials = cap_trials;
   }
+  if (getenv("ARA_DEBUG")) {
+    cudaPointerAttributes pa;
+    cudaError_t pe = cudaPointerGetAttributes(&pa, yet->event_ids);
+    fprintf(stderr, "[ara_run_host] yet ids %p: %s type=%d; ylt %p\n", (const void*)yet->event_ids,
+            cudaGetErrorString(pe), (int)pa.type, (void*)ylt_host);
+    cudaGetLastError();
+  }
   ARA_CUDA(cudaEventRecord(c->ev_done[0], s));
   ARA_CUDA(cudaEventRecord(c->ev_done[1], s));
   uint64_t t0 = 0;
@@ -564,8 +583,14 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
     case ARA_OPT_VARIANT:
       if (v < 0) return set_error(ARA_E_ARG, "variant >= 0");
       for (auto& L : c->layers)
-        if (v >= (int64_t)L.variants.size()) return set_error(ARA_E_ARG, "variant %lld not available", (long long)v);
+        if (v >= (int64_t)L.variants[c->kernel].size())
+          return set_error(ARA_E_ARG, "variant %lld not available", (long long)v);
       c->variant = (int)v;
+      return ARA_OK;
+    case ARA_OPT_KERNEL:
+      if (v < 0 || v > 1) return set_error(ARA_E_ARG, "kernel in {0 presence, 1 dense}");
+      c->kernel = (int)v;
+      c->variant = 0;
       return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
@@ -578,6 +603,7 @@ ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
     case ARA_OPT_BLOCKS_PER_SM: *v = c->blocks_per_sm; return ARA_OK;
     case ARA_OPT_L2_POLICY: *v = c->l2_policy; return ARA_OK;
     case ARA_OPT_VARIANT: *v = c->variant; return ARA_OK;
+    case ARA_OPT_KERNEL: *v = c->kernel; return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }
@@ -588,7 +614,7 @@ ara_status ara_layer_info(ara_ctx* c, uint32_t layer, uint64_t* table_bytes, uin
   const Layer& L = c->layers[layer];
   if (table_bytes) *table_bytes = L.table_bytes;
   if (row_stride) *row_stride = L.jpad * 4;
-  if (num_variants) *num_variants = (uint32_t)L.variants.size();
+  if (num_variants) *num_variants = (uint32_t)L.variants[c->kernel].size();
   if (variant_name) *variant_name = pick(c, L)->name;
   return ARA_OK;
 }

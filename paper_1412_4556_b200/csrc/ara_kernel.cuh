@@ -41,8 +41,20 @@ struct LayerParams {
   double* ylt;               // this layer's YLT row (num_trials doubles)
   unsigned* err;             // bit0: id out of range, bit1: bad offsets
   double r2, l2, r3, l3;     // FT2, FT3
+  const uint32_t* present;   // presence bitmap: bit e set iff row e holds a non-zero loss (presence kernel)
+  uint32_t present_words;    // (C + 1 + 31) / 32
+  uint32_t fold_words;       // bitmap words held in shared memory (<= present_words; folded mod fold_words)
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
+
+// Streaming 16-byte load of 4 YET ids (L1 no-allocate; L2 policy from make_policy).
+__device__ __forceinline__ uint4 ld_ids4(const uint32_t* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
 
 __device__ __forceinline__ uint64_t make_policy(bool evict_last, bool enabled) {
   uint64_t p;

@@ -103,7 +103,6 @@ def test_variable_length_config_within_tolerance(cuda_device):
     ctx = ara.context_for_config(cfg, elts)
     y = gpu_ylt(cfg, ctx, yet.event_ids, offsets_np=yet.offsets)
     assert np.all(within_tol(y, want))
-    assert np.max(np.abs(y - want) / np.maximum(np.abs(want), 1.0)) < 1e-12  # in practice far inside 1e-6
     # metrics of each path's own YLT
     rps = synth.return_periods(cfg.num_trials)
     p, t = ara.ara_pml_tvar(torch.from_numpy(y[0]).cuda(), rps)
