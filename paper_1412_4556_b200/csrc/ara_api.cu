@@ -230,6 +230,7 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
     p.present = L.present;
     p.present_words = L.present_words;
     p.fold_words = (uint32_t)std::min<int64_t>(L.present_words, budget / 4);
+    p.fold_magic = UINT64_MAX / p.fold_words + 1;
     dyn_smem = ((size_t)p.fold_words + (size_t)var->NW * kQueue) * 4;
     ARA_CUDA(cudaFuncSetAttribute((const void*)var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
   }

@@ -44,6 +44,7 @@ struct LayerParams {
   const uint32_t* present;   // presence bitmap: bit e set iff row e holds a non-zero loss (presence kernel)
   uint32_t present_words;    // (C + 1 + 31) / 32
   uint32_t fold_words;       // bitmap words held in shared memory (<= present_words; folded mod fold_words)
+  uint64_t fold_magic;       // floor((2^64 - 1) / fold_words) + 1: fast word % fold_words (Lemire)
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
 

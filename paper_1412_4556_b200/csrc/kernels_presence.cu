@@ -15,7 +15,7 @@ static const Variant kTable[] = {
     ARA_PRES(2, 1, 1, 32), ARA_PRES(2, 1, 1, 16),
     ARA_PRES(4, 1, 1, 32), ARA_PRES(4, 1, 1, 16),
     ARA_PRES(8, 1, 1, 32), ARA_PRES(8, 1, 1, 16),
-    ARA_PRES(8, 2, 1, 32), ARA_PRES(8, 2, 2, 32), ARA_PRES(8, 2, 1, 16), ARA_PRES(8, 2, 2, 16),
+    ARA_PRES(8, 2, 1, 32), ARA_PRES(8, 2, 1, 24), ARA_PRES(8, 2, 2, 32), ARA_PRES(8, 2, 1, 16),
     ARA_PRES(8, 3, 2, 32), ARA_PRES(8, 3, 4, 32),
     ARA_PRES(8, 4, 2, 32), ARA_PRES(8, 4, 4, 32),
     ARA_PRES(8, 5, 4, 32), ARA_PRES(8, 6, 4, 32), ARA_PRES(8, 7, 4, 32), ARA_PRES(8, 8, 4, 32),

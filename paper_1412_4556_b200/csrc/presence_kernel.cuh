@@ -22,52 +22,89 @@
 
 namespace ara {
 
-constexpr int kQueue = 64;  // per-warp ring of pending hits (< 32 carried + <= 32 new per slot)
+constexpr int kQueue = 128;  // per-warp ring of pending hits (< 32 carried + <= 64 new per slot pair)
 
-// Drain n (<= 32) queued events starting at ring position `head`: all 32 lanes participate.
+// Gathers for a batch of up to 32 queued events, split into an ISSUE step (loads into registers)
+// and a CONSUME step (FT1 / sum / FT2 / accumulate), so a batch's L2 latency overlaps the scan of the
+// following YET windows.  Round r covers queue slots r*32/G .. (r+1)*32/G - 1; slot r*RG + lane/G is
+// fetched by the G lanes lane/G*G .. +G-1, lane g holding vectors g, g+G, ... of the row.
 template <int V, int NV, int G>
-__device__ __forceinline__ void drain(const LayerParams& p, const uint32_t* __restrict__ q, unsigned head, int n,
-                                      int lane, const double* s_r1, const double* s_l1, uint64_t pol_tab,
-                                      double& S) {
-  constexpr int RG = 32 / G;
-  constexpr int NVL = (NV + G - 1) / G;
-  constexpr int JP = V * NV;
-  constexpr unsigned FULL = 0xffffffffu;
-  const int g = lane % G;
-#pragma unroll
-  for (int r = 0; r < G; ++r) {
+struct RowBatch {
+  static constexpr int RG = 32 / G;
+  static constexpr int NVL = (NV + G - 1) / G;
+  // Narrow rows: all G rounds of a batch stay in registers between issue and consume (async).
+  // Wide rows: one round at a time (issue and consume back to back) to stay inside 64 registers.
+  static constexpr bool kAsync = G == 1 && NVL * V <= 16;
+  static constexpr int R = kAsync ? G : 1;
+  float x[R][NVL][V];
+
+  __device__ __forceinline__ void issue_round(int r, const LayerParams& p, const uint32_t* __restrict__ q,
+                                              unsigned head, int n, int lane, uint64_t pol_tab) {
+    const int g = lane % G;
     const int slot = r * RG + lane / G;
-    if (r * RG >= n) break;  // warp-uniform
     const uint32_t id = slot < n ? q[(head + slot) & (kQueue - 1)] : 0u;
-    const float* row = p.table + (uint64_t)id * JP;
-    float x[NVL][V];
+    const float* row = p.table + (uint64_t)id * (V * NV);
+    float(&xr)[NVL][V] = x[kAsync ? r : 0];
 #pragma unroll
     for (int i = 0; i < NVL; ++i) {
       const int s = g + i * G;
       if (id != 0 && (NV % G == 0 || s < NV)) {
-        ld_row<V>(row + s * V, pol_tab, x[i]);
+        ld_row<V>(row + s * V, pol_tab, xr[i]);
       } else {
 #pragma unroll
-        for (int c = 0; c < V; ++c) x[i][c] = 0.0f;
+        for (int c = 0; c < V; ++c) xr[i][c] = 0.0f;
       }
     }
+  }
+
+  __device__ __forceinline__ void consume_round(int r, const LayerParams& p, int lane, const double* s_r1,
+                                                const double* s_l1, double& S) const {
+    const int g = lane % G;
+    const float(&xr)[NVL][V] = x[kAsync ? r : 0];
+    // Steps 1-2: FT1 on each of the row's losses, summed across the layer's ELTs.  Branch-free: an
+    // absent loss (0) gives clamp(0; R >= 0, L) = +0 exactly, so the dense sum equals the sparse one.
     double sum = 0.0;
 #pragma unroll
     for (int i = 0; i < NVL; ++i)
 #pragma unroll
       for (int c = 0; c < V; ++c) {
-        if (__float_as_uint(x[i][c]) != 0u) {
-          const int j = (g + i * G) * V + c;
-          sum += clamp_terms((double)x[i][c], s_r1[j], s_l1[j]);
-        }
+        const int j = (g + i * G) * V + c;
+        sum += clamp_terms((double)xr[i][c], s_r1[j], s_l1[j]);
       }
     if constexpr (G > 1) {
 #pragma unroll
-      for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(FULL, sum, off);
+      for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
     }
-    if (sum != 0.0 && g == 0) S += clamp_terms(sum, p.r2, p.l2);
+    if (g == 0) S += clamp_terms(sum, p.r2, p.l2);  // step 3 (FT2); step 4 accumulation (exact +0 if sum 0)
   }
-}
+
+  // Async: issue all rounds now, consume later.  Sync: issue+consume round by round.
+  __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, unsigned head, int n,
+                                        int lane, uint64_t pol_tab, const double* s_r1, const double* s_l1,
+                                        double& S) {
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      if (r * RG >= n) break;  // warp-uniform
+      issue_round(r, p, q, head, n, lane, pol_tab);
+      if constexpr (!kAsync) consume_round(r, p, lane, s_r1, s_l1, S);
+    }
+    if constexpr (kAsync) {
+      for (int r = (n + RG - 1) / RG; r < G; ++r)  // rounds past n hold nothing
+#pragma unroll
+        for (int i = 0; i < NVL; ++i)
+#pragma unroll
+          for (int c = 0; c < V; ++c) x[r][i][c] = 0.0f;
+    }
+  }
+
+  __device__ __forceinline__ void consume(const LayerParams& p, int lane, const double* s_r1, const double* s_l1,
+                                          double& S) const {
+    if constexpr (kAsync) {
+#pragma unroll
+      for (int r = 0; r < G; ++r) consume_round(r, p, lane, s_r1, s_l1, S);
+    }
+  }
+};
 
 // V/NV: row format (as ara_layer_kernel); G: lanes per row in a drain; NW: warps per block.
 template <int V, int NV, int G, int NW>
@@ -106,6 +143,19 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(p.ids) & 15u) == 0);
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t C = p.C;
+  const bool fold_sub = p.present_words <= 2u * fw;  // one conditional subtraction folds every word
+  const uint64_t fmagic = p.fold_magic;
+
+  // word index of event id in the (folded) shared bitmap
+  auto word_of = [&](uint32_t id) -> uint32_t {
+    uint32_t wd = id >> 5;
+    if (fold_sub) {
+      wd = wd >= fw ? wd - fw : wd;
+    } else {
+      wd = (uint32_t)__umul64hi(fmagic * (uint64_t)wd, (uint64_t)fw);  // wd % fw
+    }
+    return wd;
+  };
 
   for (uint64_t t = warp0; t < p.num_trials; t += nwarps) {
     uint64_t b, e;
@@ -121,63 +171,81 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       b = t * p.K;
       e = b + p.K;
     }
-    double S = 0.0;
-    unsigned head = 0;
-    int count = 0;
-    // windows of 128 ids aligned to 16 B; lane loads ids [w + 4 lane, w + 4 lane + 4)
-    uint64_t w = b & ~(uint64_t)3;
-    auto load4 = [&](uint64_t at) -> uint4 {
-      const uint64_t qq = at + 4u * lane;
+    const uint32_t len = (uint32_t)(e - b);
+    const uint32_t* base = p.ids + b;
+    // Windows of 128 ids starting at the trial's first occurrence, so the order in which hits are
+    // queued (hence the fp64 summation order) depends only on the trial's own ids: the YLT is bitwise
+    // identical however the YET is sharded or offset.  Lane l holds ids [rel + 4l, rel + 4l + 4): one
+    // 16-B vector when the trial start is 16-B aligned, else scalar loads.
+    const bool vec = vec_ok && ((b & 3u) == 0);
+    auto load4 = [&](uint32_t rel) -> uint4 {
+      const uint32_t qq = rel + 4u * lane;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (qq < e) {
-        if (vec_ok && qq + 4 <= p.num_events) {
-          v = ld_ids4(p.ids + qq, pol_yet);
+      if (qq < len) {
+        if (vec && qq + 4 <= len) {
+          v = ld_ids4(base + qq, pol_yet);
         } else {
-          v.x = ld_id(p.ids + qq, pol_yet);
-          if (qq + 1 < e) v.y = ld_id(p.ids + qq + 1, pol_yet);
-          if (qq + 2 < e) v.z = ld_id(p.ids + qq + 2, pol_yet);
-          if (qq + 3 < e) v.w = ld_id(p.ids + qq + 3, pol_yet);
+          v.x = ld_id(base + qq, pol_yet);
+          if (qq + 1 < len) v.y = ld_id(base + qq + 1, pol_yet);
+          if (qq + 2 < len) v.z = ld_id(base + qq + 2, pol_yet);
+          if (qq + 3 < len) v.w = ld_id(base + qq + 3, pol_yet);
         }
       }
       return v;
     };
-    uint4 cur = w < e ? load4(w) : make_uint4(0u, 0u, 0u, 0u);
-    for (; w < e; w += 128) {
-      const uint4 nxt = (w + 128 < e) ? load4(w + 128) : make_uint4(0u, 0u, 0u, 0u);
-      const uint32_t idv[4] = {cur.x, cur.y, cur.z, cur.w};
+    double S = 0.0;
+    unsigned head = 0;
+    unsigned count = 0;
+    RowBatch<V, NV, G> rows;
+    bool pending = false;
+    uint4 cur = load4(0);
+    uint4 nx1 = load4(128);
+    for (uint32_t rel = 0; rel < len; rel += 128) {
+      const uint4 nx2 = load4(rel + 256);
+      uint32_t id[4] = {cur.x, cur.y, cur.z, cur.w};
+      bool hit[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint64_t pos = w + 4u * lane + u;
-        uint32_t id = (pos >= b && pos < e) ? idv[u] : 0u;
-        bool hit = false;
-        if (pos >= b && pos < e) {
-          if (id - 1u >= C) {  // outside [1, C]: record, treat as absent
-            bad |= 1u;
-            id = 0u;
-          } else {
-            uint32_t wd = id >> 5;
-            if (wd >= fw) wd %= fw;
-            hit = (bits[wd] >> (id & 31u)) & 1u;
-          }
-        }
-        const unsigned m = __ballot_sync(FULL, hit);
-        if (hit) q[(head + count + __popc(m & lt)) & (kQueue - 1)] = id;
-        count += __popc(m);
-        if (count >= 32) {
+        // positions past the trial end were loaded as 0 and stay 0 (never a hit, never "bad")
+        const bool inside = rel + 4u * lane + u < len;
+        const bool ok = id[u] - 1u < C;          // 1 <= id <= C
+        bad |= (inside && !ok) ? 1u : 0u;        // outside [1, C]: record, treat as absent
+        id[u] = ok ? id[u] : 0u;                 // id 0 -> bit 0 of word 0, never set
+        const uint32_t word = bits[word_of(id[u])];
+        hit[u] = (word >> (id[u] & 31u)) & 1u;
+      }
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t ia = h ? id[2] : id[0], ib = h ? id[3] : id[1];
+        const bool ha = h ? hit[2] : hit[0], hb = h ? hit[3] : hit[1];
+        const unsigned m0 = __ballot_sync(FULL, ha);
+        const unsigned m1 = __ballot_sync(FULL, hb);
+        const unsigned n0 = __popc(m0);
+        const unsigned at = head + count;
+        if (ha) q[(at + __popc(m0 & lt)) & (kQueue - 1)] = ia;
+        if (hb) q[(at + n0 + __popc(m1 & lt)) & (kQueue - 1)] = ib;
+        count += n0 + __popc(m1);
+        while (count >= 32) {  // warp-uniform; at most 31 + 64 = 95 < kQueue pending
           __syncwarp();
-          drain<V, NV, G>(p, q, head, 32, lane, s_r1, s_l1, pol_tab, S);
+          if (pending) rows.consume(p, lane, s_r1, s_l1, S);
+          rows.issue(p, q, head, 32, lane, pol_tab, s_r1, s_l1, S);
+          pending = RowBatch<V, NV, G>::kAsync;
           __syncwarp();
           head = (head + 32) & (kQueue - 1);
           count -= 32;
         }
       }
-      cur = nxt;
+      cur = nx1;
+      nx1 = nx2;
     }
-    if (count > 0) {
+    if (count > 0) {  // final partial batch (the pending one is consumed first, in queue order)
       __syncwarp();
-      drain<V, NV, G>(p, q, head, count, lane, s_r1, s_l1, pol_tab, S);
+      if (pending) rows.consume(p, lane, s_r1, s_l1, S);
+      rows.issue(p, q, head, (int)count, lane, pol_tab, s_r1, s_l1, S);
+      pending = RowBatch<V, NV, G>::kAsync;
       __syncwarp();
     }
+    if (pending) rows.consume(p, lane, s_r1, s_l1, S);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(FULL, S, off);
     bad = __reduce_or_sync(FULL, bad);

@@ -28,7 +28,7 @@ def golden_layer(d):
 
 # ---------------------------------------------------------------- GPU-path helpers (tests only)
 def gpu_ylt(cfg_or_none, ctx, event_ids_np, offsets_np=None, K=0, num_trials=None, num_layers=1, variant=None,
-            block_threads=None, check=True):
+            block_threads=None, check=True, kernel=None):
     """Copy a host YET to the device, run ara_run, return the YLT [layers, trials] as numpy."""
     import numpy as np
     import torch
@@ -42,6 +42,8 @@ def gpu_ylt(cfg_or_none, ctx, event_ids_np, offsets_np=None, K=0, num_trials=Non
     else:
         n = num_trials if num_trials is not None else (ids.numel() // K if K else 0)
     ylt = torch.full((num_layers, max(n, 1)), -7.0, dtype=torch.float64, device=dev)
+    if kernel is not None:
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, kernel)
     if variant is not None:
         ctx.ara_set_option(ara.ARA_OPT_VARIANT, variant)
     if block_threads is not None:
@@ -76,3 +78,14 @@ def within_tol(gpu, ref, rel=1e-6, abs_floor=1e-3):
     import numpy as np
     gpu, ref = np.asarray(gpu), np.asarray(ref)
     return np.abs(gpu - ref) <= np.maximum(rel * np.abs(ref), abs_floor)
+
+
+def variants(ctx):
+    """All (kernel, variant) pairs the context can run for its layers' row width."""
+    from paper_1412_4556_b200 import ara
+    out = []
+    for k in (ara.KERNEL_PRESENCE, ara.KERNEL_DENSE):
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
+        out += [(k, v) for v in range(ctx.ara_layer_info(0)["num_variants"])]
+    ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+    return out

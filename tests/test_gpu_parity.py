@@ -12,7 +12,7 @@ import pytest
 import torch
 
 import oracle
-from ara_testutil import gpu_ylt, golden, golden_context, golden_elts, golden_layer, ragged, within_tol
+from ara_testutil import gpu_ylt, golden, golden_context, golden_elts, golden_layer, ragged, variants, within_tol
 from paper_1412_4556_b200 import ara, synth
 
 pytestmark = pytest.mark.gpu
@@ -87,11 +87,10 @@ def test_tiny_config_bitwise_all_variants_and_shapes(cuda_device):
     yet = synth.make_yet(cfg)
     want = _oracle_cfg(cfg, elts, yet)
     ctx = ara.context_for_config(cfg, elts)
-    nvar = ctx.ara_layer_info(0)["num_variants"]
-    for v in range(nvar):
+    for k, v in variants(ctx):
         for bt in (64, 256):
-            y = gpu_ylt(cfg, ctx, yet.event_ids, K=cfg.kmin, variant=v, block_threads=bt)
-            assert np.array_equal(y, want), (v, bt)
+            y = gpu_ylt(cfg, ctx, yet.event_ids, K=cfg.kmin, kernel=k, variant=v, block_threads=bt)
+            assert np.array_equal(y, want), (k, v, bt)
     assert not np.any(np.signbit(y))
 
 
@@ -138,8 +137,8 @@ def test_every_row_width_bitwise(cuda_device, J):
     C, elts, layer, yet, N, K = _small_problem(J)
     want = oracle.ylt(C, yet, None, N, K, elts, [layer])
     ctx = _ctx_from(C, elts, [layer])
-    for v in range(ctx.ara_layer_info(0)["num_variants"]):
-        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, variant=v), want), v
+    for k, v in variants(ctx):
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, kernel=k, variant=v), want), (k, v)
 
 
 @pytest.mark.parametrize("kw", [dict(inf_limits=True), dict(zero_ret=True), dict(zero_ret=True, inf_limits=True),
@@ -162,8 +161,8 @@ def test_ragged_trial_lengths(cuda_device):
     ids, off = ragged(trials)
     want = oracle.ylt(C, ids, off, len(trials), 0, elts, [layer])
     ctx = _ctx_from(C, elts, [layer])
-    for v in range(ctx.ara_layer_info(0)["num_variants"]):
-        assert np.array_equal(gpu_ylt(None, ctx, ids, offsets_np=off, variant=v), want)
+    for k, v in variants(ctx):
+        assert np.array_equal(gpu_ylt(None, ctx, ids, offsets_np=off, kernel=k, variant=v), want), (k, v)
     # offsets that do not start at 0 (a shard of a bigger YET): prefix junk ids must be ignored
     off2 = off + np.uint64(3)
     ids2 = np.concatenate([np.array([C + 5, 0, 9], np.uint32), ids])
@@ -216,6 +215,9 @@ def test_determinism_and_launch_shape_invariance_real_regime(cuda_device):
     for pol in (1, 2, 0):
         ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, pol)
         assert np.array_equal(gpu_ylt(None, ctx, yet, K=K), base)
+    for k, v in variants(ctx):  # every kernel/variant: same sums up to rounding order
+        assert np.all(within_tol(gpu_ylt(None, ctx, yet, K=K, kernel=k, variant=v), base, rel=1e-12, abs_floor=1e-6))
+    ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
     assert np.all(within_tol(base, oracle.ylt(C, yet, None, N, K, elts, [layer])))
 
 
@@ -296,3 +298,24 @@ def test_sharded_runs_reassemble_bitwise(cuda_device):
         ara.ara_unshard(gathered, G, cap, 1, starts, out)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy(), want), G
+
+
+# ------------------------------------------------------------------ presence kernel specifics
+@pytest.mark.parametrize("C,n,J", [(3_000_000, 20_000, 16),   # bitmap folded mod the shared-memory capacity
+                                   (64, 64, 5),                 # every event present: every occurrence hits
+                                   (64, 3, 2)])                 # almost nothing present
+def test_presence_fold_and_saturation(cuda_device, C, n, J):
+    C_, elts, layer, yet, N, K = _small_problem(J, C=C, n=n, N=400, K=301, seed=7)
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx_from(C, elts, [layer])
+    for k, v in variants(ctx):
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, kernel=k, variant=v), want), (k, v)
+
+
+def test_multi_layer_dense_kernel(cuda_device):
+    C, elts, layer, yet, N, K = _small_problem(24, seed=4)
+    layers = [layer, ([5, 1, 7], (100.0, 1e6), (0.0, INF)), (list(range(17)), (0.0, INF), (1e5, 2e6))]
+    want = oracle.ylt(C, yet, None, N, K, elts, layers)
+    ctx = _ctx_from(C, elts, layers)
+    for k in (ara.KERNEL_DENSE, ara.KERNEL_PRESENCE):
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_layers=len(layers), kernel=k), want), k
