@@ -352,12 +352,30 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (ara_layer_kernel, one launch per layer)
+    # ---- roofline of the dominant kernel (one launch per layer)
     occ = n_ids  # occurrences on this rank per layer pass
     row_bytes = [max(32, i["row_stride"]) for i in info]  # sector-rounded row bytes
-    alg_bytes_launch = float(np.mean([occ * (4 + rb) for rb in row_bytes]))
     launch_ms = kern_ms / L
     peak, peak_src = peaks()
+    kernel_name = info[0]["variant"].split("<")[0]
+    # compulsory HBM bytes of one presence-kernel launch: the YET ids (4 B per occurrence), the YLT
+    # row (8 B per trial), and one read of every table row that holds a loss plus the bitmap
+    present_rows = []
+    for l in cfg.layers:
+        ids_l = np.unique(np.concatenate([elts[j].event_ids for j in l.elts]))
+        present_rows.append(int(ids_l.size))
+    comp_bytes = float(np.mean([4.0 * occ + 8.0 * n_local + pr * rb + (cfg.catalog_size + 1) / 8.0
+                                for pr, rb in zip(present_rows, row_bytes)]))
+    dense_bytes = float(np.mean([occ * (4 + rb) for rb in row_bytes]))  # 4 B id + row sectors
+    if kernel_name == "ara_presence_kernel":
+        alg_bytes_launch = comp_bytes
+        alg_note = ("algorithmic bytes = compulsory HBM traffic: 4 B YET id per occurrence + 8 B YLT per trial + "
+                    "one read of each table row holding a loss (%d rows x %d B) + the presence bitmap; rows of "
+                    "events absent from every ELT are all-zero and never fetched (DESIGN.md 'Roofline')"
+                    % (present_rows[0], row_bytes[0]))
+    else:
+        alg_bytes_launch = dense_bytes
+        alg_note = "algorithmic bytes = occurrences x (4 B id + %d B sector-rounded row), SURVEY.md 8(d)" % row_bytes[0]
     achieved = alg_bytes_launch / (launch_ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_{cfg.name}.json")
@@ -366,7 +384,28 @@ def main():
             pj = json.load(f)
         if pj.get("variant") == info[0]["variant"]:
             traffic = pj.get("dram_bytes_per_launch")
-    lookups = float(sum(len(l.elts) for l in cfg.layers)) * (q1 - q0) * world  # approx total when sharded evenly
+
+    # ---- the dense direct-access kernel (every occurrence gathers its full row), timed beside
+    dense = None
+    if not args.profile and args.variant is None:
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_DENSE)
+        for _ in range(2):
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        nd = 5
+        for _ in range(nd):
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        dms = a.elapsed_time(b) / nd / L
+        dense = {"kernel": ctx.ara_layer_info(0)["variant"], "launch_ms": dms,
+                 "achieved_GBps": dense_bytes / (dms * 1e-3) / 1e9, "frac": dense_bytes / (dms * 1e-3) / 1e9 / peak,
+                 "alg_bytes_per_launch": dense_bytes,
+                 "note": "SURVEY.md 8(d) definition: occurrences x (4 B id + sector-rounded row); table gathers are "
+                         "served mostly from DRAM (ncu: L2 hit ~36%)"}
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+        ctx.ara_check(stream)
     lookups_exact = float(sum(len(l.elts) for l in cfg.layers)) * (
         N * cfg.kmin if cfg.fixed_length else float(synth.trial_offsets(cfg.seed, N, cfg.kmin, cfg.kmax)[-1]))
     value = ms_per_step * 1e6 / N
@@ -386,10 +425,11 @@ def main():
         "elt_lookups_per_s": lookups_exact / (ms_per_step * 1e-3),
         "kernel_ms_per_step": kern_ms, "create_ms": create_ms, "cold_l2_ms_per_step": cold_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "ara_layer_kernel",
+                     "traffic": traffic, "kernel": kernel_name,
                      "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": launch_ms,
-                     "note": f"algorithmic bytes = occurrences x (4 B id + {row_bytes[0]} B sector-rounded row); "
-                             f"peak {peak_src}; the table is L2-resident so this is an effective-bandwidth fraction"},
+                     "effective_GBps_68B": dense_bytes / (launch_ms * 1e-3) / 1e9,
+                     "note": alg_note + f"; peak {peak_src}"},
+        "dense_kernel": dense,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps * (L + n_metric_launches),

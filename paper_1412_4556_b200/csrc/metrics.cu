@@ -89,14 +89,17 @@ __global__ void __launch_bounds__(kSelBlock) select_pass(const double* __restric
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // Last block: pull the global histograms into shared memory in parallel, then one thread per query
+  // walks its 256 bins from the top (digit 255) to find the bucket holding its remaining rank.
+  for (int i = threadIdx.x; i < nq * 256; i += blockDim.x) sh[i / 256][i % 256] = ((volatile unsigned int*)st->hist[i / 256])[i % 256];
+  __syncthreads();
   if (threadIdx.x < m) {
     const int q = threadIdx.x;
-    const int hq = pass == 0 ? 0 : q;
-    volatile unsigned int* h = st->hist[hq];
+    const unsigned int* h = sh[pass == 0 ? 0 : q];
     uint64_t r = st->rank[q], above = 0;
     int d = 255;
     for (; d > 0; --d) {
-      uint64_t c = h[d];
+      const uint64_t c = h[d];
       if (above + c >= r) break;
       above += c;
     }
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(kSelBlock) select_pass(const double* __restric
     st->prefix[q] = (st->prefix[q] << 8) | (uint64_t)d;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kMaxQ * 256; i += blockDim.x) st->hist[i / 256][i % 256] = 0;
+  for (int i = threadIdx.x; i < nq * 256; i += blockDim.x) st->hist[i / 256][i % 256] = 0;
   if (threadIdx.x == 0) st->ticket = 0;
 }
 
@@ -169,13 +172,34 @@ __global__ void __launch_bounds__(kSelBlock) tail_pass(const double* __restrict_
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // Last block: every warp sums a strided subset of the block partials for each query (fixed order),
+  // then warp partials are combined in warp order -- deterministic.
+  __shared__ double fsum[kSelBlock / 32][kMaxQ];
+  __shared__ unsigned long long fcnt[kSelBlock / 32][kMaxQ];
+  for (int q = 0; q < m; ++q) {
+    double a = 0.0;
+    unsigned long long b = 0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+      a += ((volatile double*)psum)[(uint64_t)i * kMaxQ + q];
+      b += ((volatile unsigned long long*)pcnt)[(uint64_t)i * kMaxQ + q];
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+      b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    if (lane == 0) {
+      fsum[w][q] = a;
+      fcnt[w][q] = b;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x < m) {
     const int q = threadIdx.x;
     double a = 0.0;
     unsigned long long b = 0;
-    for (unsigned i = 0; i < gridDim.x; ++i) {
-      a += ((volatile double*)psum)[(uint64_t)i * kMaxQ + q];
-      b += ((volatile unsigned long long*)pcnt)[(uint64_t)i * kMaxQ + q];
+    for (int i = 0; i < kSelBlock / 32; ++i) {
+      a += fsum[i][q];
+      b += fcnt[i][q];
     }
     const double T = from_key(sT[q]);
     const uint64_t k = st->k[q];

@@ -112,15 +112,18 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   constexpr int JP = V * NV;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ uint32_t smem[];
-  __shared__ double s_r1[JP], s_l1[JP];
+  // FT1 terms, padded to the G*NVL*V columns a row group covers (padding: R = 0, L = +inf, so the
+  // branch-free FT1 of a padding column -- always loss 0 -- is exactly +0).
+  constexpr int JPS = G * ((NV + G - 1) / G) * V;
+  __shared__ double s_r1[JPS], s_l1[JPS];
   uint32_t* bits = smem;                       // [fold_words]
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint32_t* q = smem + p.fold_words + warp * kQueue;
 
-  for (int j = threadIdx.x; j < JP; j += blockDim.x) {
-    s_r1[j] = p.r1[j];
-    s_l1[j] = p.l1[j];
+  for (int j = threadIdx.x; j < JPS; j += blockDim.x) {
+    s_r1[j] = j < JP ? p.r1[j] : 0.0;
+    s_l1[j] = j < JP ? p.l1[j] : __longlong_as_double(0x7ff0000000000000ll);
   }
   // Stage the presence bitmap (folded modulo fold_words if it does not fit).
   const uint32_t fw = p.fold_words;
