@@ -103,6 +103,25 @@ __device__ __forceinline__ double clamp_terms(double x, double R, double L) {
   return (y < L) ? y : L;
 }
 
+// Same clamp, branch- and NaN-handling-free (inputs are never NaN): max(y, 0) by masking the sign with
+// integer ops, then one compare-select against the limit.  Bitwise identical to clamp_terms for every
+// non-NaN input (x - R is never -0.0 here; a negative difference becomes +0).
+__device__ __forceinline__ double clamp_fast(double x, double R, double L) {
+  const double y = x - R;
+  const int hi = __double2hiint(y), lo = __double2loint(y);
+  const int keep = ~(hi >> 31);
+  const double z = __hiloint2double(hi & keep, lo & keep);
+  double r;
+  asm("{\n .reg .pred p;\n setp.lt.f64 p, %1, %2;\n selp.f64 %0, %1, %2, p;\n}" : "=d"(r) : "d"(z), "d"(L));
+  return r;
+}
+
+// st.shared predicated on `pred` without a branch.
+__device__ __forceinline__ void st_shared_if(uint32_t* ptr, uint32_t v, bool pred) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.shared.u32 [%0], %1;\n}"
+               :: "r"((uint32_t)__cvta_generic_to_shared(ptr)), "r"(v), "r"((int)pred) : "memory");
+}
+
 // V: floats per vector load; NV: vectors per row (jpad = V*NV); G: lanes per row (power of 2 <= 32);
 // U: rows per row group per iteration.
 template <int V, int NV, int G, int U>

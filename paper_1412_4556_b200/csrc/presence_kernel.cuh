@@ -42,13 +42,16 @@ struct RowBatch {
                                               unsigned head, int n, int lane, uint64_t pol_tab) {
     const int g = lane % G;
     const int slot = r * RG + lane / G;
-    const uint32_t id = slot < n ? q[(head + slot) & (kQueue - 1)] : 0u;
+    // queue word = parity tag (bit 31) | event id; an id > C (invalid input that hit a folded bitmap
+    // word) fetches the zero row 0 instead
+    uint32_t id = slot < n ? (q[(head + slot) & (kQueue - 1)] & 0x7fffffffu) : 0u;
+    id = id <= p.C ? id : 0u;
     const float* row = p.table + (uint64_t)id * (V * NV);
     float(&xr)[NVL][V] = x[kAsync ? r : 0];
 #pragma unroll
     for (int i = 0; i < NVL; ++i) {
       const int s = g + i * G;
-      if (id != 0 && (NV % G == 0 || s < NV)) {
+      if (NV % G == 0 || s < NV) {  // empty slots fetch row 0, a real all-zero row
         ld_row<V>(row + s * V, pol_tab, xr[i]);
       } else {
 #pragma unroll
@@ -69,13 +72,26 @@ struct RowBatch {
 #pragma unroll
       for (int c = 0; c < V; ++c) {
         const int j = (g + i * G) * V + c;
-        sum += clamp_terms((double)xr[i][c], s_r1[j], s_l1[j]);
+        sum += clamp_fast((double)xr[i][c], s_r1[j], s_l1[j]);
       }
     if constexpr (G > 1) {
 #pragma unroll
       for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
     }
-    if (g == 0) S += clamp_terms(sum, p.r2, p.l2);  // step 3 (FT2); step 4 accumulation (exact +0 if sum 0)
+    if (g == 0) S += clamp_fast(sum, p.r2, p.l2);  // step 3 (FT2); step 4 accumulation (exact +0 if sum 0)
+  }
+
+  // G == 1 only: occurrence-net loss o = FT2(sum_j FT1(x_j)) of the lane's own row (slot = lane).
+  __device__ __forceinline__ double row_loss(const LayerParams& p, const double* s_r1, const double* s_l1) const {
+    double sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < NVL; ++i)
+#pragma unroll
+      for (int c = 0; c < V; ++c) {
+        const int j = i * V + c;
+        sum += clamp_fast((double)x[0][i][c], s_r1[j], s_l1[j]);  // steps 1-2
+      }
+    return clamp_fast(sum, p.r2, p.l2);  // step 3 (exactly +0 for an all-zero row)
   }
 
   // Async: issue all rounds now, consume later.  Sync: issue+consume round by round.
@@ -106,20 +122,40 @@ struct RowBatch {
   }
 };
 
-// V/NV: row format (as ara_layer_kernel); G: lanes per row in a drain; NW: warps per block.
+// Per-warp bookkeeping of the (at most two) trials whose hits are still in flight (carried queue).
+struct WarpTrials {
+  uint64_t trial[2];  // trial index per parity slot
+  uint32_t first[2];  // stream position of the trial's first hit
+  uint32_t end[2];    // stream position one past its last hit (valid once its scan is done)
+  uint32_t state[2];  // 0 free, 1 scanning, 2 scanned (waiting for its hits to be consumed)
+  uint32_t bad;
+};
+
+// V/NV: row format (as ara_layer_kernel); G: lanes per row in a batch; NW: warps per block.
+//
+// Hits are queued as (trial parity << 31 | event id) and, for narrow rows (G == 1), the queue is CARRIED
+// across the warp's consecutive trials: batches are always full (32 rows) except when the queue must be
+// flushed, so the per-trial partial batch disappears.  The occurrence-net loss of the i-th hit of a
+// trial is always accumulated by lane i mod 32 (a shuffle rotates each batch into that frame), and the
+// lanes are combined by the same xor-tree -- so a trial's fp64 summation order depends only on its own
+// ids, never on its neighbours, the sharding or the launch shape.
 template <int V, int NV, int G, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_constant__ LayerParams p) {
   constexpr int JP = V * NV;
   constexpr unsigned FULL = 0xffffffffu;
+  using Batch = RowBatch<V, NV, G>;
+  constexpr bool kCarry = (G == 1) && Batch::kAsync;
   extern __shared__ uint32_t smem[];
   // FT1 terms, padded to the G*NVL*V columns a row group covers (padding: R = 0, L = +inf, so the
   // branch-free FT1 of a padding column -- always loss 0 -- is exactly +0).
   constexpr int JPS = G * ((NV + G - 1) / G) * V;
   __shared__ double s_r1[JPS], s_l1[JPS];
-  uint32_t* bits = smem;                       // [fold_words]
+  __shared__ WarpTrials s_wt[NW];
+  uint32_t* bits = smem;  // [fold_words]
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint32_t* q = smem + p.fold_words + warp * kQueue;
+  WarpTrials& wt = s_wt[warp];
 
   for (int j = threadIdx.x; j < JPS; j += blockDim.x) {
     s_r1[j] = j < JP ? p.r1[j] : 0.0;
@@ -137,32 +173,99 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       if (v) atomicOr(&bits[w % fw], v);
     }
   }
+  if (lane == 0) {
+    wt.state[0] = wt.state[1] = 0u;
+    wt.bad = 0u;
+  }
   __syncthreads();
 
   const uint64_t pol_tab = make_policy(true, p.l2_hints);
   const uint64_t pol_yet = make_policy(false, p.l2_hints);
-  const uint64_t warp0 = (uint64_t)blockIdx.x * NW + warp;
-  const uint64_t nwarps = (uint64_t)gridDim.x * NW;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(p.ids) & 15u) == 0);
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t C = p.C;
-  const bool fold_sub = p.present_words <= 2u * fw;  // one conditional subtraction folds every word
+  const bool fold_small = p.present_words <= 2u * fw;  // one conditional subtraction folds every word
   const uint64_t fmagic = p.fold_magic;
+  const bool carry = kCarry && (C < 0x80000000u);      // the parity tag lives in bit 31 of a queue word
 
-  // word index of event id in the (folded) shared bitmap
-  auto word_of = [&](uint32_t id) -> uint32_t {
-    uint32_t wd = id >> 5;
-    if (fold_sub) {
-      wd = wd >= fw ? wd - fw : wd;
+  double S0 = 0.0, S1 = 0.0;  // per-lane partial sums of the (<= 2) open trials, by parity
+  unsigned head = 0, count = 0;  // ring of queued, not yet issued hits
+  uint32_t issued = 0;           // stream position of the next hit to issue
+  Batch rows;
+  uint32_t bstart = 0, btag = 0; // pending batch: stream position of slot 0; this lane's entry tag
+  int bn = 0;                    // pending batch size (0 = none)
+
+  // FT3 on the warp-combined sum of parity slot a; lane 0 writes the YLT.
+  auto finalize = [&](int a) {
+    double S = (kCarry && a) ? S1 : S0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(FULL, S, off);
+    if (lane == 0) p.ylt[wt.trial[a]] = clamp_terms(S, p.r3, p.l3);  // step 4: aggregate terms FT3
+    if (kCarry && a) S1 = 0.0; else S0 = 0.0;
+    __syncwarp();
+    if (lane == 0) wt.state[a] = 0u;
+    __syncwarp();
+  };
+  // Consume the pending batch: FT1/FT2 per row, rotate each trial's share into its canonical lanes.
+  auto consume = [&]() {
+    if (bn == 0) return;
+    if constexpr (kCarry) {
+      const double o = rows.row_loss(p, s_r1, s_l1);
+      const bool mine = lane < bn;
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        if (wt.state[a] == 0u) continue;  // warp-uniform
+        const int src = (int)((uint32_t)lane + wt.first[a] - bstart) & 31;
+        const double oa = __shfl_sync(FULL, o, src);
+        const bool ok = __shfl_sync(FULL, mine && btag == (uint32_t)a, src);
+        if (ok) {
+          if (a) S1 += oa; else S0 += oa;
+        }
+      }
     } else {
-      wd = (uint32_t)__umul64hi(fmagic * (uint64_t)wd, (uint64_t)fw);  // wd % fw
+      rows.consume(p, lane, s_r1, s_l1, S0);
     }
-    return wd;
+    const uint32_t done = bstart + (uint32_t)bn;
+    bn = 0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+      if (wt.state[a] == 2u && (int32_t)(done - wt.end[a]) >= 0) finalize(a);
+  };
+  // Issue the next n (<= 32) queued hits as a batch (consuming the previous batch first).
+  auto issue = [&](int n) {
+    consume();
+    __syncwarp();
+    const uint32_t word = lane < n ? q[(head + lane) & (kQueue - 1)] : 0u;
+    btag = word >> 31;
+    rows.issue(p, q, head, n, lane, pol_tab, s_r1, s_l1, S0);
+    __syncwarp();
+    bstart = issued;
+    bn = n;
+    issued += (uint32_t)n;
+    head = (head + (unsigned)n) & (kQueue - 1);
+    count -= (unsigned)n;
+    if constexpr (!kCarry) consume();  // wide rows: rows.issue already consumed round by round
+  };
+  auto flush = [&]() {
+    while (count > 0) issue(count < 32 ? (int)count : 32);
+    consume();
   };
 
-  for (uint64_t t = warp0; t < p.num_trials; t += nwarps) {
+  unsigned bad = 0;
+  uint32_t k = 0;    // local trial counter (parity = k & 1)
+  for (uint64_t t = (uint64_t)blockIdx.x * NW + warp; t < p.num_trials; t += (uint64_t)gridDim.x * NW, ++k) {
+    const int par = (int)(k & 1u);
+    if (wt.state[par] != 0u) flush();  // trial k-2 still has hits in flight
+    __syncwarp();
+    if (lane == 0) {
+      wt.trial[par] = t;
+      wt.first[par] = issued + count;  // stream position of the trial's first hit
+      wt.state[par] = 1u;
+    }
+    __syncwarp();
+    const uint32_t tag = (uint32_t)par << 31;
+
     uint64_t b, e;
-    unsigned bad = 0;
     if (p.offsets) {
       b = p.offsets[t];
       e = p.offsets[t + 1];
@@ -176,13 +279,12 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     }
     const uint32_t len = (uint32_t)(e - b);
     const uint32_t* base = p.ids + b;
-    // Windows of 128 ids starting at the trial's first occurrence, so the order in which hits are
-    // queued (hence the fp64 summation order) depends only on the trial's own ids: the YLT is bitwise
-    // identical however the YET is sharded or offset.  Lane l holds ids [rel + 4l, rel + 4l + 4): one
-    // 16-B vector when the trial start is 16-B aligned, else scalar loads.
+    // Windows of 128 ids from the trial's first occurrence; lane l holds ids [rel + 4l, rel + 4l + 4):
+    // one 16-B vector when the trial start is 16-B aligned, else scalar loads.  Ids past the end read 0.
     const bool vec = vec_ok && ((b & 3u) == 0);
     auto load4 = [&](uint32_t rel) -> uint4 {
       const uint32_t qq = rel + 4u * lane;
+      if (vec && rel + 128 <= len) return ld_ids4(base + qq, pol_yet);  // warp-uniform fast path
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
       if (qq < len) {
         if (vec && qq + 4 <= len) {
@@ -196,67 +298,61 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       }
       return v;
     };
-    double S = 0.0;
-    unsigned head = 0;
-    unsigned count = 0;
-    RowBatch<V, NV, G> rows;
-    bool pending = false;
     uint4 cur = load4(0);
     uint4 nx1 = load4(128);
     for (uint32_t rel = 0; rel < len; rel += 128) {
       const uint4 nx2 = load4(rel + 256);
-      uint32_t id[4] = {cur.x, cur.y, cur.z, cur.w};
+      const uint32_t id[4] = {cur.x, cur.y, cur.z, cur.w};
+      // validity: every id of the window in [1, C] (positions past the end hold 0 and are excused)
+      if (rel + 128 <= len) {
+        const uint32_t mn = min(min(id[0], id[1]), min(id[2], id[3]));
+        const uint32_t mx = max(max(id[0], id[1]), max(id[2], id[3]));
+        bad |= (mn == 0u || mx > C) ? 1u : 0u;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) bad |= (rel + 4u * lane + u < len && id[u] - 1u >= C) ? 1u : 0u;
+      }
       bool hit[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        // positions past the trial end were loaded as 0 and stay 0 (never a hit, never "bad")
-        const bool inside = rel + 4u * lane + u < len;
-        const bool ok = id[u] - 1u < C;          // 1 <= id <= C
-        bad |= (inside && !ok) ? 1u : 0u;        // outside [1, C]: record, treat as absent
-        id[u] = ok ? id[u] : 0u;                 // id 0 -> bit 0 of word 0, never set
-        const uint32_t word = bits[word_of(id[u])];
-        hit[u] = (word >> (id[u] & 31u)) & 1u;
+        uint32_t wd = min(id[u], C) >> 5;  // an invalid id > C is clamped into the bitmap
+        wd = fold_small ? min(wd, wd - fw) : (uint32_t)__umul64hi(fmagic * (uint64_t)wd, (uint64_t)fw);
+        hit[u] = (bits[wd] >> (id[u] & 31u)) & 1u;  // id 0 -> bit 0 of word 0, never set
       }
-#pragma unroll 1
+#pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const uint32_t ia = h ? id[2] : id[0], ib = h ? id[3] : id[1];
-        const bool ha = h ? hit[2] : hit[0], hb = h ? hit[3] : hit[1];
-        const unsigned m0 = __ballot_sync(FULL, ha);
-        const unsigned m1 = __ballot_sync(FULL, hb);
+        const unsigned m0 = __ballot_sync(FULL, hit[2 * h]);
+        const unsigned m1 = __ballot_sync(FULL, hit[2 * h + 1]);
         const unsigned n0 = __popc(m0);
         const unsigned at = head + count;
-        if (ha) q[(at + __popc(m0 & lt)) & (kQueue - 1)] = ia;
-        if (hb) q[(at + n0 + __popc(m1 & lt)) & (kQueue - 1)] = ib;
+        st_shared_if(q + ((at + __popc(m0 & lt)) & (kQueue - 1)), tag | id[2 * h], hit[2 * h]);
+        st_shared_if(q + ((at + n0 + __popc(m1 & lt)) & (kQueue - 1)), tag | id[2 * h + 1], hit[2 * h + 1]);
         count += n0 + __popc(m1);
-        while (count >= 32) {  // warp-uniform; at most 31 + 64 = 95 < kQueue pending
-          __syncwarp();
-          if (pending) rows.consume(p, lane, s_r1, s_l1, S);
-          rows.issue(p, q, head, 32, lane, pol_tab, s_r1, s_l1, S);
-          pending = RowBatch<V, NV, G>::kAsync;
-          __syncwarp();
-          head = (head + 32) & (kQueue - 1);
-          count -= 32;
-        }
+        while (count >= 32) issue(32);  // warp-uniform; at most 31 + 64 = 95 < kQueue queued
       }
       cur = nx1;
       nx1 = nx2;
     }
-    if (count > 0) {  // final partial batch (the pending one is consumed first, in queue order)
-      __syncwarp();
-      if (pending) rows.consume(p, lane, s_r1, s_l1, S);
-      rows.issue(p, q, head, (int)count, lane, pol_tab, s_r1, s_l1, S);
-      pending = RowBatch<V, NV, G>::kAsync;
-      __syncwarp();
-    }
-    if (pending) rows.consume(p, lane, s_r1, s_l1, S);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(FULL, S, off);
-    bad = __reduce_or_sync(FULL, bad);
+    __syncwarp();
     if (lane == 0) {
-      p.ylt[t] = clamp_terms(S, p.r3, p.l3);
-      if (bad) atomicOr(p.err, bad);
+      wt.end[par] = issued + count;
+      wt.state[par] = 2u;
+    }
+    __syncwarp();
+    if (!carry) {
+      flush();
+    } else if (count == 0 && bn == 0) {
+      // nothing of this trial in flight (e.g. no hits at all): finalize now
+      for (int a = 0; a < 2; ++a)
+        if (wt.state[a] == 2u && (int32_t)(issued - wt.end[a]) >= 0) finalize(a);
     }
   }
+  flush();
+  // a trial with no hits after the last flush is already finalized by consume()/the check above
+  for (int a = 0; a < 2; ++a)
+    if (wt.state[a] == 2u) finalize(a);
+  bad = __reduce_or_sync(FULL, bad);
+  if (lane == 0 && bad) atomicOr(p.err, bad);
 }
 
 }  // namespace ara
