@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--config", default="P")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", type=int, default=None)
+    ap.add_argument("--kernel", default=None, choices=["presence", "dense"], help="force the ARA kernel kind")
     ap.add_argument("--block", type=int, default=None)
     ap.add_argument("--bps", type=int, default=None)
     ap.add_argument("--l2-policy", type=int, default=None)
@@ -195,6 +196,8 @@ def main():
     c0 = time.perf_counter()
     ctx = ara.context_for_config(cfg, elts, device=dev.index, stream=stream)
     create_ms = (time.perf_counter() - c0) * 1e3
+    if args.kernel is not None:
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_DENSE if args.kernel == "dense" else ara.KERNEL_PRESENCE)
     if args.variant is not None:
         ctx.ara_set_option(ara.ARA_OPT_VARIANT, args.variant)
     if args.block is not None:
@@ -387,7 +390,7 @@ def main():
 
     # ---- the dense direct-access kernel (every occurrence gathers its full row), timed beside
     dense = None
-    if not args.profile and args.variant is None:
+    if not args.profile and args.variant is None and kernel_name == "ara_presence_kernel":
         ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_DENSE)
         for _ in range(2):
             ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)

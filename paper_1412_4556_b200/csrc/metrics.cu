@@ -28,8 +28,11 @@ struct SelState {
   uint64_t prefix[kMaxQ];  // known high bits of the k-th largest key (right-aligned)
   uint64_t rank[kMaxQ];    // remaining 1-based rank from the top among keys sharing the prefix
   uint64_t k[kMaxQ];
-  unsigned int hist[kMaxQ][256];
+  unsigned int hist[kMaxQ][256];  // per histogram SLOT (distinct prefix), not per query
   unsigned int ticket;
+  int nslot;                      // distinct prefixes this pass; queries sharing one share a histogram
+  int q2slot[kMaxQ];
+  uint64_t slot_prefix[kMaxQ];
   double sum[kMaxQ];       // filled by the tail pass
   unsigned long long cnt[kMaxQ];
 };
@@ -45,42 +48,42 @@ __device__ __forceinline__ double from_key(uint64_t k) {
   return __longlong_as_double((long long)b);
 }
 
-// One radix pass: histogram of digit `pass` (bits 63-8*pass .. 56-8*pass) over the keys that match
-// each query's prefix; the last block picks each query's digit.
+// One radix pass: histogram of digit `pass` (bits 63-8*pass .. 56-8*pass) over the keys that match each
+// distinct query prefix (queries with equal prefixes share one histogram slot); the last block picks
+// each query's digit and rebuilds the slots for the next pass.
 __global__ void __launch_bounds__(kSelBlock) select_pass(const double* __restrict__ y, uint64_t n, int m, int pass,
                                                           SelState* st) {
   __shared__ unsigned int sh[kMaxQ][256];
   __shared__ uint64_t spre[kMaxQ];
+  __shared__ int s_nslot;
   __shared__ bool last;
-  for (int i = threadIdx.x; i < m * 256; i += blockDim.x) sh[i / 256][i % 256] = 0;
-  if (threadIdx.x < m) spre[threadIdx.x] = st->prefix[threadIdx.x];
+  if (threadIdx.x == 0) s_nslot = st->nslot;
+  if (threadIdx.x < kMaxQ) spre[threadIdx.x] = st->slot_prefix[threadIdx.x];
+  __syncthreads();
+  const int ns = s_nslot;
+  for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) sh[i / 256][i % 256] = 0;
   __syncthreads();
   const int shift = 56 - 8 * pass;
   const unsigned FULL = 0xffffffffu;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   // Iterate in warp-uniform trip counts so __match_any_sync sees the whole warp.
-  const uint64_t base0 = (uint64_t)blockIdx.x * blockDim.x;
-  for (uint64_t base = base0; base < n; base += stride) {
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint64_t i = base + threadIdx.x;
     const bool valid = i < n;
     const uint64_t key = valid ? to_key(y[i]) : 0;
     const unsigned digit = (unsigned)(key >> shift) & 0xffu;
     const uint64_t hi = pass == 0 ? 0 : (key >> (shift + 8));
-    for (int q = 0; q < m; ++q) {
-      const bool hit = valid && hi == spre[q];
+    for (int sl = 0; sl < ns; ++sl) {
+      const bool hit = valid && hi == spre[sl];
       if (!__any_sync(FULL, hit)) continue;
       const unsigned tag = hit ? digit : 0x100u;
       const unsigned peers = __match_any_sync(FULL, tag);
-      if (hit && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&sh[q][digit], __popc(peers));
-      if (pass == 0) {  // all prefixes are empty: one histogram serves every query
-        break;
-      }
+      if (hit && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&sh[sl][digit], __popc(peers));
     }
   }
   __syncthreads();
-  const int nq = pass == 0 ? 1 : m;
-  for (int i = threadIdx.x; i < nq * 256; i += blockDim.x) {
-    unsigned v = sh[i / 256][i % 256];
+  for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) {
+    const unsigned v = sh[i / 256][i % 256];
     if (v) atomicAdd(&st->hist[i / 256][i % 256], v);
   }
   __threadfence();
@@ -90,12 +93,12 @@ __global__ void __launch_bounds__(kSelBlock) select_pass(const double* __restric
   if (!last) return;
   __threadfence();
   // Last block: pull the global histograms into shared memory in parallel, then one thread per query
-  // walks its 256 bins from the top (digit 255) to find the bucket holding its remaining rank.
-  for (int i = threadIdx.x; i < nq * 256; i += blockDim.x) sh[i / 256][i % 256] = ((volatile unsigned int*)st->hist[i / 256])[i % 256];
+  // walks its slot's 256 bins from the top (digit 255) to find the bucket holding its remaining rank.
+  for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) sh[i / 256][i % 256] = ((volatile unsigned int*)st->hist[i / 256])[i % 256];
   __syncthreads();
   if (threadIdx.x < m) {
     const int q = threadIdx.x;
-    const unsigned int* h = sh[pass == 0 ? 0 : q];
+    const unsigned int* h = sh[st->q2slot[q]];
     uint64_t r = st->rank[q], above = 0;
     int d = 255;
     for (; d > 0; --d) {
@@ -107,8 +110,19 @@ __global__ void __launch_bounds__(kSelBlock) select_pass(const double* __restric
     st->prefix[q] = (st->prefix[q] << 8) | (uint64_t)d;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nq * 256; i += blockDim.x) st->hist[i / 256][i % 256] = 0;
-  if (threadIdx.x == 0) st->ticket = 0;
+  for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) st->hist[i / 256][i % 256] = 0;
+  if (threadIdx.x == 0) {
+    int k = 0;  // distinct prefixes for the next pass, in query order
+    for (int q = 0; q < m; ++q) {
+      const uint64_t pq = st->prefix[q];
+      int sl = 0;
+      while (sl < k && st->slot_prefix[sl] != pq) ++sl;
+      if (sl == k) st->slot_prefix[k++] = pq;
+      st->q2slot[q] = sl;
+    }
+    st->nslot = k;
+    st->ticket = 0;
+  }
 }
 
 // Tail pass: per query, count and fp64-sum the values with key > T (T = full prefix after 8 passes).
@@ -255,7 +269,10 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
     for (int q = 0; q < mq; ++q) {
       init.rank[q] = ks[q0 + q];
       init.k[q] = ks[q0 + q];
+      init.q2slot[q] = 0;
     }
+    init.nslot = 1;  // pass 0: every prefix is empty
+    init.slot_prefix[0] = 0;
     cudaError_t e = cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s);
     for (int pass = 0; pass < 8 && e == cudaSuccess; ++pass) {
       select_pass<<<(unsigned)blocks, kSelBlock, 0, s>>>(ylt, n, mq, pass, st);

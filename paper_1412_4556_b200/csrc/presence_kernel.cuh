@@ -206,30 +206,34 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     if (lane == 0) wt.state[a] = 0u;
     __syncwarp();
   };
-  // Consume the pending batch: FT1/FT2 per row, rotate each trial's share into its canonical lanes.
-  auto consume = [&]() {
-    if (bn == 0) return;
-    if constexpr (kCarry) {
-      const double o = rows.row_loss(p, s_r1, s_l1);
-      const bool mine = lane < bn;
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        if (wt.state[a] == 0u) continue;  // warp-uniform
-        const int src = (int)((uint32_t)lane + wt.first[a] - bstart) & 31;
-        const double oa = __shfl_sync(FULL, o, src);
-        const bool ok = __shfl_sync(FULL, mine && btag == (uint32_t)a, src);
-        if (ok) {
-          if (a) S1 += oa; else S0 += oa;
-        }
-      }
-    } else {
-      rows.consume(p, lane, s_r1, s_l1, S0);
-    }
-    const uint32_t done = bstart + (uint32_t)bn;
-    bn = 0;
+  // Finalize every scanned trial whose hits have all been consumed (stream position `done`).
+  auto settle = [&](uint32_t done) {
 #pragma unroll
     for (int a = 0; a < 2; ++a)
       if (wt.state[a] == 2u && (int32_t)(done - wt.end[a]) >= 0) finalize(a);
+  };
+  // Consume the pending batch: FT1/FT2 per row, rotate each trial's share into its canonical lanes.
+  auto consume = [&]() {
+    if (bn != 0) {
+      if constexpr (kCarry) {
+        const double o = rows.row_loss(p, s_r1, s_l1);
+        const bool mine = lane < bn;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          if (wt.state[a] == 0u) continue;  // warp-uniform
+          const int src = (int)((uint32_t)lane + wt.first[a] - bstart) & 31;
+          const double oa = __shfl_sync(FULL, o, src);
+          const bool ok = __shfl_sync(FULL, mine && btag == (uint32_t)a, src);
+          if (ok) {
+            if (a) S1 += oa; else S0 += oa;
+          }
+        }
+      } else {
+        rows.consume(p, lane, s_r1, s_l1, S0);
+      }
+      bn = 0;
+    }
+    settle(issued);  // every issued hit is consumed now
   };
   // Issue the next n (<= 32) queued hits as a batch (consuming the previous batch first).
   auto issue = [&](int n) {
@@ -340,11 +344,9 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     }
     __syncwarp();
     if (!carry) {
-      flush();
-    } else if (count == 0 && bn == 0) {
-      // nothing of this trial in flight (e.g. no hits at all): finalize now
-      for (int a = 0; a < 2; ++a)
-        if (wt.state[a] == 2u && (int32_t)(issued - wt.end[a]) >= 0) finalize(a);
+      flush();  // wide rows: one trial at a time (finalized by the flush's settle)
+    } else if (bn == 0) {
+      settle(issued);  // nothing pending: a trial with no outstanding hits is final now
     }
   }
   flush();

@@ -319,3 +319,33 @@ def test_multi_layer_dense_kernel(cuda_device):
     ctx = _ctx_from(C, elts, layers)
     for k in (ara.KERNEL_DENSE, ara.KERNEL_PRESENCE):
         assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_layers=len(layers), kernel=k), want), k
+
+
+@pytest.mark.parametrize("J", [2, 16, 24, 100])
+@pytest.mark.parametrize("C", [1000, 3_000_000, 10_000_000])
+def test_trials_with_hit_counts_at_batch_boundaries(cuda_device, J, C):
+    """Trials whose number of present events is 0, 1, 31, 32, 33, 64, 96 ... (batch-size multiples),
+    in every order; C = 10M also exercises the large-fold (modulo) bitmap path."""
+    rng = np.random.default_rng(J * 7 + C % 97)
+    present = np.arange(1, 51, dtype=np.uint32)           # events that hold losses
+    elts = []
+    for j in range(J):
+        ids = rng.choice(present, size=rng.integers(1, 51), replace=False).astype(np.uint32)
+        elts.append((ids, (rng.integers(1, 1 << 20, size=ids.size)).astype(np.float32),
+                     (float(rng.integers(0, 1 << 12)), INF if j % 2 else float(1 << 21))))
+    # make every present id hit at least one ELT
+    elts[0] = (present, (rng.integers(1, 1 << 20, size=50)).astype(np.float32), (0.0, INF))
+    layer = (list(range(J)), (100.0, 1e7), (500.0, 1e9))
+    K = 160
+    hits = [0, 1, 31, 32, 33, 64, 96, 0, 32, 0, 63, 65, 128, 160, 0]
+    trials = []
+    for h in hits * 3:
+        t = np.concatenate([rng.choice(present, size=h), rng.integers(51, C + 1, size=K - h)]).astype(np.uint32)
+        rng.shuffle(t)
+        trials.append(t)
+    yet = np.concatenate(trials)
+    N = len(trials)
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx_from(C, elts, [layer])
+    for k, v in variants(ctx):
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, kernel=k, variant=v), want), (k, v)
