@@ -363,10 +363,7 @@ def main():
     kernel_name = info[0]["variant"].split("<")[0]
     # compulsory HBM bytes of one presence-kernel launch: the YET ids (4 B per occurrence), the YLT
     # row (8 B per trial), and one read of every table row that holds a loss plus the bitmap
-    present_rows = []
-    for l in cfg.layers:
-        ids_l = np.unique(np.concatenate([elts[j].event_ids for j in l.elts]))
-        present_rows.append(int(ids_l.size))
+    present_rows = [ctx.ara_layer_stats(l)["present_rows"] for l in range(L)]
     comp_bytes = float(np.mean([4.0 * occ + 8.0 * n_local + pr * rb + (cfg.catalog_size + 1) / 8.0
                                 for pr, rb in zip(present_rows, row_bytes)]))
     dense_bytes = float(np.mean([occ * (4 + rb) for rb in row_bytes]))  # 4 B id + row sectors
@@ -407,7 +404,7 @@ def main():
                  "alg_bytes_per_launch": dense_bytes,
                  "note": "SURVEY.md 8(d) definition: occurrences x (4 B id + sector-rounded row); table gathers are "
                          "served mostly from DRAM (ncu: L2 hit ~36%)"}
-        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_AUTO)
         ctx.ara_check(stream)
     lookups_exact = float(sum(len(l.elts) for l in cfg.layers)) * (
         N * cfg.kmin if cfg.fixed_length else float(synth.trial_offsets(cfg.seed, N, cfg.kmin, cfg.kmax)[-1]))

@@ -160,8 +160,11 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           1 no hints, 2 hints + persisting access-policy window on the table
  *   ARA_OPT_VARIANT         kernel variant index within the selected kernel and row width
  *                           (ara_layer_info reports the count)
- *   ARA_OPT_KERNEL          0 presence (default): a per-layer presence bitmap of the table's non-zero
- *                           rows, staged in shared memory, so only rows that hold a loss are gathered;
+ *   ARA_OPT_KERNEL          -1 auto (default): per layer, the presence kernel when its folded bitmap is
+ *                           expected to send at most 25% of the occurrences (15% for J > 16) to the
+ *                           row gather, else the dense kernel;
+ *                           0 presence: a per-layer presence bitmap of the table's non-zero rows,
+ *                           staged in shared memory, so only rows that hold a loss are gathered;
  *                           1 dense: every occurrence gathers its full row.  Identical results (an
  *                           all-zero row contributes exactly 0, reading c9).
  *                           Selecting a kernel resets ARA_OPT_VARIANT to 0.
@@ -180,6 +183,13 @@ ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);
  * variants for its J, and a description of the selected variant (static string). */
 ARA_API ara_status ara_layer_info(ara_ctx* ctx, uint32_t layer, uint64_t* table_bytes, uint32_t* row_stride,
                           uint32_t* num_variants, const char** variant_name);
+
+/* Presence statistics of layer l (computed by ara_create on the host): rows of the table that hold at
+ * least one loss, the expected share of occurrences the presence kernel sends to the row gather (its
+ * folded shared-memory bitmap), and the kernel that runs for this layer under the current
+ * ARA_OPT_KERNEL (0 presence, 1 dense).  Any output pointer may be NULL. */
+ARA_API ara_status ara_layer_stats(ara_ctx* ctx, uint32_t layer, uint64_t* present_rows, double* est_hit_rate,
+                                   int* kernel);
 
 /* Test hook: copy row `event` of layer l's table (row_stride bytes) to HOST out.  Synchronous. */
 ARA_API ara_status ara_table_row(ara_ctx* ctx, uint32_t layer, uint32_t event, float* out);

@@ -22,13 +22,13 @@ LIB_PATH = os.path.join(_HERE, "libara.so")
 
 ARA_OK, ARA_E_ARG, ARA_E_RANGE, ARA_E_DUP, ARA_E_VALUE, ARA_E_NOMEM, ARA_E_CUDA, ARA_E_UNSUPPORTED = range(8)
 ARA_OPT_BLOCK_THREADS, ARA_OPT_BLOCKS_PER_SM, ARA_OPT_L2_POLICY, ARA_OPT_VARIANT, ARA_OPT_KERNEL = 1, 2, 3, 4, 5
-KERNEL_PRESENCE, KERNEL_DENSE = 0, 1
+KERNEL_AUTO, KERNEL_PRESENCE, KERNEL_DENSE = -1, 0, 1
 ARA_MAX_ELTS_PER_LAYER = 128
 
 #: every symbol include/ara.h declares (checked by tests/test_abi.py against the header and the .so)
 EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_host", "ara_check", "ara_pml_tvar", "ara_pml",
            "ara_tvar", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
-           "ara_layer_info", "ara_table_row", "ara_status_string", "ara_last_error", "ara_version")
+           "ara_layer_info", "ara_layer_stats", "ara_table_row", "ara_status_string", "ara_last_error", "ara_version")
 
 
 class AraError(RuntimeError):
@@ -83,6 +83,8 @@ def lib() -> ctypes.CDLL:
             "ara_get_option": (st, [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]),
             "ara_layer_info": (st, [vp, u32, ctypes.POINTER(u64), ctypes.POINTER(u32), ctypes.POINTER(u32),
                                     ctypes.POINTER(ctypes.c_char_p)]),
+            "ara_layer_stats": (st, [vp, u32, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_int)]),
             "ara_table_row": (st, [vp, u32, u32, dp]),
             "ara_status_string": (ctypes.c_char_p, [ctypes.c_int]),
             "ara_last_error": (ctypes.c_char_p, []),
@@ -242,6 +244,12 @@ class Context:
         _check(lib().ara_layer_info(self._h, layer, ctypes.byref(b), ctypes.byref(s), ctypes.byref(nv),
                                     ctypes.byref(name)), "ara_layer_info")
         return {"table_bytes": b.value, "row_stride": s.value, "num_variants": nv.value, "variant": name.value.decode()}
+
+    def ara_layer_stats(self, layer: int = 0) -> dict:
+        pr, hr, k = ctypes.c_uint64(), ctypes.c_double(), ctypes.c_int()
+        _check(lib().ara_layer_stats(self._h, layer, ctypes.byref(pr), ctypes.byref(hr), ctypes.byref(k)),
+               "ara_layer_stats")
+        return {"present_rows": pr.value, "est_hit_rate": hr.value, "kernel": k.value}
 
     def ara_table_row(self, layer: int, event: int) -> np.ndarray:
         stride = self.ara_layer_info(layer)["row_stride"]

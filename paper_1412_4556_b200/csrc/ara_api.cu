@@ -62,6 +62,9 @@ struct Layer {
   uint32_t* present = nullptr;  // presence bitmap, (C + 1 + 31) / 32 words
   uint32_t present_words = 0;
   std::vector<const Variant*> variants[2];  // by KernelKind
+  uint64_t present_rows = 0;                // rows holding at least one loss
+  double est_hit_rate = 0.0;                // expected share of occurrences gathered by the presence kernel
+  int auto_kind = KIND_PRESENCE;            // kernel chosen when ARA_OPT_KERNEL is auto
   double r1[kMaxJ], l1[kMaxJ];
   double r2 = 0, l2 = 0, r3 = 0, l3 = 0;
 };
@@ -80,7 +83,7 @@ struct ara_ctx {
   int blocks_per_sm = 0;
   int l2_policy = 0;
   int variant = 0;
-  int kernel = 0;  // KernelKind
+  int kernel = -1;  // KernelKind, or -1 = per-layer automatic choice
   int persist_max = 0, window_max = 0;
   int smem_optin = 0;
   // end-to-end host path
@@ -186,8 +189,10 @@ static void destroy_ctx(ara_ctx* c) {
   delete c;
 }
 
+static int kind_of(const ara_ctx* c, const Layer& L) { return c->kernel < 0 ? L.auto_kind : c->kernel; }
+
 static const Variant* pick(const ara_ctx* c, const Layer& L) {
-  const auto& vs = L.variants[c->kernel];
+  const auto& vs = L.variants[kind_of(c, L)];
   int v = c->variant;
   if (v < 0 || v >= (int)vs.size()) v = 0;
   return vs[v];
@@ -392,6 +397,25 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       FAIL(set_error(ARA_E_NOMEM, "presence bitmap for layer %u", l));
     }
     CK(cudaMemsetAsync(L.present, 0, (size_t)L.present_words * 4, s));
+    {  // presence statistics -> automatic kernel choice (see ara.h, ARA_OPT_KERNEL)
+      std::vector<uint64_t> row((catalog_size + 64ull) / 64, 0);
+      for (uint32_t m = 0; m < L.J; ++m) {
+        const ara_elt& e = elts[in.elt_index[m]];
+        for (uint64_t i = 0; i < e.num_entries; ++i) row[e.event_ids[i] >> 6] |= 1ull << (e.event_ids[i] & 63);
+      }
+      for (uint64_t w : row) L.present_rows += (uint64_t)__builtin_popcountll(w);
+      const Variant* pv = L.variants[KIND_PRESENCE][0];
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, (const void*)pv->fn));
+      const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)pv->NW * kQueue * 4;
+      const double pw = (double)(((uint64_t)catalog_size + 1 + 31) / 32);
+      const double fw = budget > 0 ? std::min(pw, (double)(budget / 4)) : 1.0;
+      const double dens = (double)L.present_rows / ((double)catalog_size + 1.0);
+      L.est_hit_rate = 1.0 - pow(1.0 - dens, std::max(1.0, pw / fw));
+      // the presence kernel pays off while it skips most rows; wide rows (J > 16) gather 13+ sectors
+      // per hit in round-by-round batches, so they need a sparser bitmap
+      L.auto_kind = (budget >= 4096 && L.est_hit_rate <= (L.jpad <= 16 ? 0.25 : 0.15)) ? KIND_PRESENCE : KIND_DENSE;
+    }
     h_ids.clear();
     h_col.clear();
     h_loss.clear();
@@ -584,12 +608,12 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
     case ARA_OPT_VARIANT:
       if (v < 0) return set_error(ARA_E_ARG, "variant >= 0");
       for (auto& L : c->layers)
-        if (v >= (int64_t)L.variants[c->kernel].size())
+        if (v >= (int64_t)L.variants[kind_of(c, L)].size())
           return set_error(ARA_E_ARG, "variant %lld not available", (long long)v);
       c->variant = (int)v;
       return ARA_OK;
     case ARA_OPT_KERNEL:
-      if (v < 0 || v > 1) return set_error(ARA_E_ARG, "kernel in {0 presence, 1 dense}");
+      if (v < -1 || v > 1) return set_error(ARA_E_ARG, "kernel in {-1 auto, 0 presence, 1 dense}");
       c->kernel = (int)v;
       c->variant = 0;
       return ARA_OK;
@@ -615,8 +639,17 @@ ara_status ara_layer_info(ara_ctx* c, uint32_t layer, uint64_t* table_bytes, uin
   const Layer& L = c->layers[layer];
   if (table_bytes) *table_bytes = L.table_bytes;
   if (row_stride) *row_stride = L.jpad * 4;
-  if (num_variants) *num_variants = (uint32_t)L.variants[c->kernel].size();
+  if (num_variants) *num_variants = (uint32_t)L.variants[kind_of(c, L)].size();
   if (variant_name) *variant_name = pick(c, L)->name;
+  return ARA_OK;
+}
+
+ara_status ara_layer_stats(ara_ctx* c, uint32_t layer, uint64_t* present_rows, double* est_hit_rate, int* kernel) {
+  if (!c || layer >= c->layers.size()) return set_error(ARA_E_ARG, "invalid context or layer");
+  const Layer& L = c->layers[layer];
+  if (present_rows) *present_rows = L.present_rows;
+  if (est_hit_rate) *est_hit_rate = L.est_hit_rate;
+  if (kernel) *kernel = kind_of(c, L);
   return ARA_OK;
 }
 

@@ -87,5 +87,5 @@ def variants(ctx):
     for k in (ara.KERNEL_PRESENCE, ara.KERNEL_DENSE):
         ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
         out += [(k, v) for v in range(ctx.ara_layer_info(0)["num_variants"])]
-    ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+    ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_AUTO)
     return out

@@ -217,7 +217,7 @@ def test_determinism_and_launch_shape_invariance_real_regime(cuda_device):
         assert np.array_equal(gpu_ylt(None, ctx, yet, K=K), base)
     for k, v in variants(ctx):  # every kernel/variant: same sums up to rounding order
         assert np.all(within_tol(gpu_ylt(None, ctx, yet, K=K, kernel=k, variant=v), base, rel=1e-12, abs_floor=1e-6))
-    ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+    ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_AUTO)
     assert np.all(within_tol(base, oracle.ylt(C, yet, None, N, K, elts, [layer])))
 
 
@@ -349,3 +349,17 @@ def test_trials_with_hit_counts_at_batch_boundaries(cuda_device, J, C):
     ctx = _ctx_from(C, elts, [layer])
     for k, v in variants(ctx):
         assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, kernel=k, variant=v), want), (k, v)
+
+
+def test_automatic_kernel_choice(cuda_device):
+    """ARA_OPT_KERNEL auto: presence kernel for the paper-shaped layer (sparse bitmap), dense kernel when the
+    folded bitmap would send most occurrences to the gather (10M-event catalogue, 100 ELTs)."""
+    for name, want in (("T", ara.KERNEL_PRESENCE), ("P", ara.KERNEL_PRESENCE), ("X", ara.KERNEL_DENSE)):
+        cfg = synth.Config.load(name)
+        ctx = ara.context_for_config(cfg, synth.make_elts(cfg))
+        st = ctx.ara_layer_stats(0)
+        assert st["kernel"] == want, (name, st)
+        assert 0 < st["est_hit_rate"] <= 1
+        ids = np.unique(np.concatenate([e for e in (synth.make_elts(cfg)[j].event_ids for j in cfg.layers[0].elts)]))
+        assert st["present_rows"] == ids.size
+        ctx.close()
