@@ -12,7 +12,10 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
+
+#include <algorithm>
 
 #include <vector>
 
@@ -223,6 +226,240 @@ __global__ void __launch_bounds__(kSelBlock) tail_pass(const double* __restrict_
   if (threadIdx.x == 0) st->ticket = 0;
 }
 
+// ------------------------------------------------------------------------------------------------
+// Fused variant: ONE cooperative launch runs the 8 radix passes and the tail pass, separated by grid
+// barriers.  Each block keeps its contiguous chunk of keys in shared memory (when it fits), so the
+// YLT is read from HBM once; every block redundantly derives the per-query digits from the final
+// global histogram of the pass (triple-buffered so it can be cleared two passes ahead).
+constexpr int kFusedBlock = 256;
+constexpr int kCacheKeys = 4096;  // 32 KB of cached keys per block
+
+struct FusedState {
+  unsigned int H[3][kMaxQ][256];
+  unsigned int bar_count, bar_gen;
+  uint64_t k[kMaxQ];
+};
+
+__device__ __forceinline__ void grid_sync(unsigned int* count, unsigned int* gen, unsigned int nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = gen;
+    const unsigned int g = *vgen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nb - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __restrict__ y, uint64_t n, int m,
+                                                              FusedState* st, double* __restrict__ psum,
+                                                              unsigned long long* __restrict__ pcnt,
+                                                              double* __restrict__ out) {
+  extern __shared__ uint64_t skeys[];
+  __shared__ unsigned int sh[kMaxQ][256];
+  __shared__ uint64_t s_prefix[kMaxQ], s_rank[kMaxQ], s_slot_prefix[kMaxQ];
+  __shared__ int s_q2slot[kMaxQ], s_nslot;
+  __shared__ double wsum[kFusedBlock / 32][kMaxQ];
+  __shared__ unsigned long long wcnt[kFusedBlock / 32][kMaxQ];
+  const unsigned FULL = 0xffffffffu;
+  const unsigned nb = gridDim.x;
+  const uint64_t lo = n * blockIdx.x / nb, hi = n * (blockIdx.x + 1) / nb;
+  const uint32_t cnt = (uint32_t)(hi - lo);
+  const bool cached = (n + nb - 1) / nb <= (uint64_t)kCacheKeys;  // uniform over blocks
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (cached)
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) skeys[i] = to_key(y[lo + i]);
+  if (threadIdx.x < m) {
+    s_prefix[threadIdx.x] = 0;
+    s_rank[threadIdx.x] = st->k[threadIdx.x];
+    s_q2slot[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) {
+    s_nslot = 1;
+    s_slot_prefix[0] = 0;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 8; ++pass) {
+    const int ns = s_nslot;
+    for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) sh[i / 256][i % 256] = 0;
+    __syncthreads();
+    const int shift = 56 - 8 * pass;
+    for (uint32_t base = 0; base < cnt; base += blockDim.x) {  // warp-uniform trip count
+      const uint32_t i = base + threadIdx.x;
+      const bool valid = i < cnt;
+      const uint64_t key = valid ? (cached ? skeys[i] : to_key(y[lo + i])) : 0;
+      const unsigned digit = (unsigned)(key >> shift) & 0xffu;
+      const uint64_t hik = pass == 0 ? 0 : (key >> (shift + 8));
+      for (int sl = 0; sl < ns; ++sl) {
+        const bool hit = valid && hik == s_slot_prefix[sl];
+        if (!__any_sync(FULL, hit)) continue;
+        const unsigned peers = __match_any_sync(FULL, hit ? digit : 0x100u);
+        if (hit && (__ffs(peers) - 1) == lane) atomicAdd(&sh[sl][digit], __popc(peers));
+      }
+    }
+    __syncthreads();
+    unsigned int(*H)[256] = st->H[pass % 3];
+    for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) {
+      const unsigned v = sh[i / 256][i % 256];
+      if (v) atomicAdd(&H[i / 256][i % 256], v);
+    }
+    if (blockIdx.x == 0)  // clear the buffer pass+1 will use (last read before the previous barrier)
+      for (int i = threadIdx.x; i < kMaxQ * 256; i += blockDim.x) st->H[(pass + 1) % 3][i / 256][i % 256] = 0;
+    grid_sync(&st->bar_count, &st->bar_gen, nb);
+    for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) sh[i / 256][i % 256] = ((volatile unsigned int*)H[i / 256])[i % 256];
+    __syncthreads();
+    if (threadIdx.x < m) {
+      const int q = threadIdx.x;
+      const unsigned int* h = sh[s_q2slot[q]];
+      uint64_t r = s_rank[q], above = 0;
+      int d = 255;
+      for (; d > 0; --d) {
+        const uint64_t c = h[d];
+        if (above + c >= r) break;
+        above += c;
+      }
+      s_rank[q] = r - above;
+      s_prefix[q] = (s_prefix[q] << 8) | (uint64_t)d;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (int q = 0; q < m; ++q) {
+        int sl = 0;
+        while (sl < k && s_slot_prefix[sl] != s_prefix[q]) ++sl;
+        if (sl == k) s_slot_prefix[k++] = s_prefix[q];
+        s_q2slot[q] = sl;
+      }
+      s_nslot = k;
+    }
+    __syncthreads();
+  }
+  // tail: count and fp64-sum the values above each query's threshold T (fixed reduction order)
+  double sacc[kMaxQ];
+  unsigned long long cacc[kMaxQ];
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) {
+    sacc[q] = 0.0;
+    cacc[q] = 0;
+  }
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint64_t key = cached ? skeys[i] : to_key(y[lo + i]);
+    const double v = from_key(key);
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q)
+      if (q < m && key > s_prefix[q]) {
+        sacc[q] += v;
+        cacc[q] += 1;
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) {
+    if (q >= m) break;
+    double a = sacc[q];
+    unsigned long long b = cacc[q];
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(FULL, a, off);
+      b += __shfl_xor_sync(FULL, b, off);
+    }
+    if (lane == 0) {
+      wsum[w][q] = a;
+      wcnt[w][q] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < m) {
+    double a = 0.0;
+    unsigned long long b = 0;
+    for (int i = 0; i < kFusedBlock / 32; ++i) {
+      a += wsum[i][threadIdx.x];
+      b += wcnt[i][threadIdx.x];
+    }
+    psum[(uint64_t)blockIdx.x * kMaxQ + threadIdx.x] = a;
+    pcnt[(uint64_t)blockIdx.x * kMaxQ + threadIdx.x] = b;
+  }
+  grid_sync(&st->bar_count, &st->bar_gen, nb);
+  if (blockIdx.x != 0) return;
+  for (int q = 0; q < m; ++q) {
+    double a = 0.0;
+    unsigned long long b = 0;
+    for (unsigned i = threadIdx.x; i < nb; i += blockDim.x) {
+      a += ((volatile double*)psum)[(uint64_t)i * kMaxQ + q];
+      b += ((volatile unsigned long long*)pcnt)[(uint64_t)i * kMaxQ + q];
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(FULL, a, off);
+      b += __shfl_xor_sync(FULL, b, off);
+    }
+    if (lane == 0) {
+      wsum[w][q] = a;
+      wcnt[w][q] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < m) {
+    const int q = threadIdx.x;
+    double a = 0.0;
+    unsigned long long b = 0;
+    for (int i = 0; i < kFusedBlock / 32; ++i) {
+      a += wsum[i][q];
+      b += wcnt[i][q];
+    }
+    const double T = from_key(s_prefix[q]);
+    const uint64_t k = st->k[q];
+    out[q] = T;
+    out[kMaxQ + q] = __ddiv_rn(__dadd_rn(a, __dmul_rn((double)(k - b), T)), (double)k);
+  }
+}
+
+// Launch the fused kernel cooperatively for one batch of <= kMaxQ queries; returns false if the
+// device refuses a cooperative launch of the needed size (caller falls back to the pass kernels).
+static bool metrics_fused_batch(const double* ylt, uint64_t n, int mq, const uint64_t* ks, char* scratch,
+                                size_t scratch_bytes, double* h_out, cudaStream_t s, cudaError_t* err) {
+  int dev = 0, sms = 148, occ = 0;
+  *err = cudaSuccess;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return false;
+  const size_t dyn = (size_t)kCacheKeys * sizeof(uint64_t);
+  cudaFuncSetAttribute((const void*)metrics_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)metrics_fused, kFusedBlock, dyn) != cudaSuccess ||
+      occ < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  uint64_t grid = (uint64_t)sms * occ;
+  const uint64_t need = (n + kFusedBlock - 1) / kFusedBlock;
+  if (grid > need) grid = need;
+  const size_t state = sizeof(FusedState);
+  const size_t need_bytes = state + grid * kMaxQ * (sizeof(double) + sizeof(unsigned long long)) + 2 * kMaxQ * sizeof(double);
+  if (need_bytes > scratch_bytes) return false;
+  FusedState* st = (FusedState*)scratch;
+  double* psum = (double*)(scratch + state);
+  unsigned long long* pcnt = (unsigned long long*)(psum + grid * kMaxQ);
+  double* d_out = (double*)(pcnt + grid * kMaxQ);
+  FusedState init;
+  memset(&init, 0, sizeof init);
+  for (int q = 0; q < mq; ++q) init.k[q] = ks[q];
+  if ((*err = cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s)) != cudaSuccess) return true;
+  int m_ = mq;
+  void* args[] = {(void*)&ylt, (void*)&n, (void*)&m_, (void*)&st, (void*)&psum, (void*)&pcnt, (void*)&d_out};
+  if ((*err = cudaLaunchCooperativeKernel((const void*)metrics_fused, dim3((unsigned)grid), dim3(kFusedBlock), args, dyn, s)) !=
+      cudaSuccess)
+    return true;
+  if ((*err = cudaMemcpyAsync(h_out, d_out, 2 * kMaxQ * sizeof(double), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return true;
+  *err = cudaStreamSynchronize(s);
+  return true;
+}
+
 // k = ceil(n / RP) (reading c12): exact integer ceil for integral RP, fuzzed otherwise.  0 = invalid.
 static uint64_t metric_rank(uint64_t n, double rp) {
   if (!(rp > 1.0) || !(rp <= (double)n) || !isfinite(rp)) return 0;
@@ -236,6 +473,7 @@ static uint64_t metric_rank(uint64_t n, double rp) {
 
 static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml, double* tvar,
                           cudaStream_t s) {
+  const bool use_fused = getenv("ARA_METRICS_PASSES") == nullptr;  // env switch keeps the pass kernels testable
   if (!ylt || !rps || n == 0 || m == 0 || m > ARA_MAX_RETURN_PERIODS)
     return set_error(ARA_E_ARG, "invalid metric arguments");
   std::vector<uint64_t> ks(m);
@@ -247,13 +485,13 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
   ARA_CUDA(cudaGetDevice(&dev));
   ARA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   uint64_t blocks = (n + kSelBlock - 1) / kSelBlock;
-  if (blocks > (uint64_t)sms * 4) blocks = (uint64_t)sms * 4;
+  if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;  // covers the fused grid (<= SMs x occupancy)
   SelState* st = nullptr;
   double* psum = nullptr;
   unsigned long long* pcnt = nullptr;
   double* d_out = nullptr;
-  const size_t bytes = sizeof(SelState) + blocks * kMaxQ * (sizeof(double) + sizeof(unsigned long long)) +
-                       2 * kMaxQ * sizeof(double);
+  const size_t bytes = std::max(sizeof(SelState), sizeof(FusedState)) +
+                       blocks * kMaxQ * (sizeof(double) + sizeof(unsigned long long)) + 2 * kMaxQ * sizeof(double);
   char* scratch = nullptr;
   ARA_CUDA(cudaMallocAsync((void**)&scratch, bytes, s));
   st = (SelState*)scratch;
@@ -273,7 +511,19 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
     }
     init.nslot = 1;  // pass 0: every prefix is empty
     init.slot_prefix[0] = 0;
-    cudaError_t e = cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaSuccess;
+    if (use_fused && metrics_fused_batch(ylt, n, mq, &ks[q0], scratch, bytes, h_out.data(), s, &e)) {
+      if (e != cudaSuccess) {
+        rc = cuda_error(e, "fused metric kernel");
+        break;
+      }
+      for (int q = 0; q < mq; ++q) {
+        if (pml) pml[q0 + q] = h_out[q];
+        if (tvar) tvar[q0 + q] = h_out[kMaxQ + q];
+      }
+      continue;
+    }
+    e = cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s);
     for (int pass = 0; pass < 8 && e == cudaSuccess; ++pass) {
       select_pass<<<(unsigned)blocks, kSelBlock, 0, s>>>(ylt, n, mq, pass, st);
       e = cudaGetLastError();

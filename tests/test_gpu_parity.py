@@ -363,3 +363,22 @@ def test_automatic_kernel_choice(cuda_device):
         ids = np.unique(np.concatenate([e for e in (synth.make_elts(cfg)[j].event_ids for j in cfg.layers[0].elts)]))
         assert st["present_rows"] == ids.size
         ctx.close()
+
+
+def test_metrics_fused_and_pass_kernels_agree(cuda_device, monkeypatch):
+    """The cooperative fused metric kernel and the 8+1 pass kernels return identical results."""
+    rng = np.random.default_rng(21)
+    for n in (1, 7, 1000, 300_001, 2_000_000):
+        y = np.floor(rng.exponential(1e6, n)) * (rng.random(n) > 0.3)
+        y[rng.random(n) < 0.1] = 4e6
+        rps = [r for r in synth.return_periods(max(n, 2)) if r <= n] or ([float(n)] if n > 1 else [])
+        if not rps:
+            continue
+        d = torch.from_numpy(y).cuda()
+        monkeypatch.delenv("ARA_METRICS_PASSES", raising=False)
+        p1, t1 = ara.ara_pml_tvar(d, rps)
+        monkeypatch.setenv("ARA_METRICS_PASSES", "1")
+        p2, t2 = ara.ara_pml_tvar(d, rps)
+        monkeypatch.delenv("ARA_METRICS_PASSES")
+        assert np.array_equal(p1, p2) and np.array_equal(p1, oracle.pml(y, rps)), n
+        assert np.array_equal(t1, oracle.tvar(y, rps)) and np.array_equal(t2, t1), n
