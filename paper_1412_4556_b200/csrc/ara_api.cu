@@ -60,6 +60,7 @@ struct Layer {
   float* table = nullptr;
   uint64_t table_bytes = 0;
   uint32_t* present = nullptr;  // presence bitmap, (C + 1 + 31) / 32 words
+  uint4* rec = nullptr;         // sparse row records (C + 1) x 16 B, rows of <= 16 columns
   uint32_t present_words = 0;
   std::vector<const Variant*> variants[2];  // by KernelKind
   uint64_t present_rows = 0;                // rows holding at least one loss
@@ -167,6 +168,29 @@ __global__ void __launch_bounds__(256) presence_build_kernel(uint32_t* __restric
 }
 
 
+// Sparse record per table row (see ld_rec in ara_kernel.cuh): the first two non-zero columns and losses
+// and the count of non-zero columns.
+__global__ void __launch_bounds__(256) record_build_kernel(uint4* __restrict__ rec, const float* __restrict__ table,
+                                                           uint32_t jpad, uint64_t rows) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows; e += (uint64_t)gridDim.x * blockDim.x) {
+    const float* row = table + e * jpad;
+    uint32_t n = 0, c1 = 0, c2 = 0, l1 = 0, l2 = 0;
+    for (uint32_t j = 0; j < jpad; ++j) {
+      const uint32_t b = __float_as_uint(row[j]);
+      if (b == 0u) continue;
+      if (n == 0) {
+        c1 = j;
+        l1 = b;
+      } else if (n == 1) {
+        c2 = j;
+        l2 = b;
+      }
+      ++n;
+    }
+    rec[e] = make_uint4(c1 | (c2 << 8) | (n << 16), l1, l2, 0u);
+  }
+}
+
 static void destroy_ctx(ara_ctx* c) {
   if (!c) return;
   DeviceGuard guard(c->device);
@@ -174,6 +198,7 @@ static void destroy_ctx(ara_ctx* c) {
   for (auto& L : c->layers) {
     cudaFree(L.table);
     cudaFree(L.present);
+    cudaFree(L.rec);
   }
   cudaFree(c->d_err);
   cudaFreeHost(c->h_err);
@@ -233,6 +258,7 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
     const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)var->NW * kQueue * 4;
     if (budget < 4096) return set_error(ARA_E_UNSUPPORTED, "no shared memory left for the presence bitmap");
     p.present = L.present;
+    p.rec = L.rec;
     p.present_words = L.present_words;
     p.fold_words = (uint32_t)std::min<int64_t>(L.present_words, budget / 4);
     p.fold_magic = UINT64_MAX / p.fold_words + 1;
@@ -438,6 +464,16 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       CK(cudaGetLastError());
       presence_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(L.present, d_ids, n);
       CK(cudaGetLastError());
+      if (L.jpad <= 16) {  // sparse records for the narrow-row presence kernel
+        if (cudaMalloc(&L.rec, ((uint64_t)catalog_size + 1) * sizeof(uint4)) != cudaSuccess) {
+          cudaGetLastError();
+          FAIL(set_error(ARA_E_NOMEM, "row records for layer %u", l));
+        }
+        const uint64_t rows = (uint64_t)catalog_size + 1;
+        const uint64_t rb = std::min<uint64_t>((rows + 255) / 256, (uint64_t)c->sms * 16);
+        record_build_kernel<<<(unsigned)rb, 256, 0, s>>>(L.rec, L.table, L.jpad, rows);
+        CK(cudaGetLastError());
+      }
       CK(cudaStreamSynchronize(s));  // host staging vectors are reused for the next layer
       cudaFree(d_ids);
       cudaFree(d_col);

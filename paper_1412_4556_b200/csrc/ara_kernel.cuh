@@ -45,8 +45,21 @@ struct LayerParams {
   uint32_t present_words;    // (C + 1 + 31) / 32
   uint32_t fold_words;       // bitmap words held in shared memory (<= present_words; folded mod fold_words)
   uint64_t fold_magic;       // floor((2^64 - 1) / fold_words) + 1: fast word % fold_words (Lemire)
+  const uint4* rec;          // per-event sparse row record (presence kernel, rows <= 16 columns)
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
+
+// Sparse record of one table row (built by ara_create for rows of <= 16 columns):
+//   x = c1 | c2 << 8 | n << 16   (n = non-zero losses in the row; c1 < c2 their columns, layer order)
+//   y = bits of the loss in column c1 (0 if n == 0), z = bits of the loss in column c2 (0 if n < 2)
+// A row with n > 2 is read in full from the table.
+__device__ __forceinline__ uint4 ld_rec(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
 
 // Streaming 16-byte load of 4 YET ids (L1 no-allocate; L2 policy from make_policy).
 __device__ __forceinline__ uint4 ld_ids4(const uint32_t* p, uint64_t pol) {

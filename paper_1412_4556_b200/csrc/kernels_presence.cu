@@ -11,11 +11,11 @@ namespace ara {
 
 static const Variant kTable[] = {
     // ---- presence-bitmap kernels (default path); first per row width = default (B200 sweeps)
-    ARA_PRES(1, 1, 1, 24), ARA_PRES(1, 1, 1, 32), ARA_PRES(1, 1, 1, 16),
-    ARA_PRES(2, 1, 1, 24), ARA_PRES(2, 1, 1, 32), ARA_PRES(2, 1, 1, 16),
-    ARA_PRES(4, 1, 1, 24), ARA_PRES(4, 1, 1, 32), ARA_PRES(4, 1, 1, 16),
-    ARA_PRES(8, 1, 1, 24), ARA_PRES(8, 1, 1, 32), ARA_PRES(8, 1, 1, 16),
-    ARA_PRES(8, 2, 1, 24), ARA_PRES(8, 2, 1, 32), ARA_PRES(8, 2, 1, 16), ARA_PRES(8, 2, 2, 24),
+    ARA_PRES(1, 1, 1, 32), ARA_PRES(1, 1, 1, 24), ARA_PRES(1, 1, 1, 16),
+    ARA_PRES(2, 1, 1, 32), ARA_PRES(2, 1, 1, 24), ARA_PRES(2, 1, 1, 16),
+    ARA_PRES(4, 1, 1, 32), ARA_PRES(4, 1, 1, 24), ARA_PRES(4, 1, 1, 16),
+    ARA_PRES(8, 1, 1, 32), ARA_PRES(8, 1, 1, 24), ARA_PRES(8, 1, 1, 16),
+    ARA_PRES(8, 2, 1, 32), ARA_PRES(8, 2, 1, 24), ARA_PRES(8, 2, 1, 16), ARA_PRES(8, 2, 2, 24),
     ARA_PRES(8, 3, 2, 16), ARA_PRES(8, 3, 4, 16), ARA_PRES(8, 3, 2, 24),
     ARA_PRES(8, 4, 2, 16), ARA_PRES(8, 4, 4, 16), ARA_PRES(8, 4, 2, 24),
     ARA_PRES(8, 5, 16, 16), ARA_PRES(8, 5, 8, 16), ARA_PRES(8, 5, 16, 24),

@@ -122,6 +122,60 @@ struct RowBatch {
   }
 };
 
+// Narrow rows (<= 16 columns, one lane per row): the batch holds each queued event's 16-byte sparse
+// RECORD instead of its full row.  Typically a present row has a single non-zero loss (the ELTs are
+// sparse and nearly disjoint), so steps 1-3 cost two FT1 clamps and one FT2 clamp per row; a row with
+// more than two losses (rare) is read in full from the table.  The sum runs over the non-zero columns
+// in layer order, i.e. the oracle's order with its exact +0 terms dropped.
+template <int V, int NV>
+struct RecBatch {
+  static constexpr bool kAsync = true;
+  uint4 r;
+  uint32_t id;
+
+  __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, unsigned head, int n,
+                                        int lane, uint64_t pol_tab) {
+    uint32_t e = lane < n ? (q[(head + lane) & (kQueue - 1)] & 0x7fffffffu) : 0u;
+    id = e <= p.C ? e : 0u;  // invalid ids (folded-bitmap collisions) read the zero record of row 0
+    r = ld_rec(p.rec + id, pol_tab);
+  }
+
+  // occurrence-net loss o = FT2(sum_j FT1(x_j)) of the lane's queued event
+  __device__ __forceinline__ double row_loss(const LayerParams& p, const double* s_r1, const double* s_l1,
+                                             uint64_t pol_tab) const {
+    const uint32_t c1 = r.x & 0xffu, c2 = (r.x >> 8) & 0xffu, nz = (r.x >> 16) & 0xffu;
+    double sum = 0.0;
+    if (__any_sync(0xffffffffu, nz > 2u)) {  // rare: some row of the batch has more than two losses
+      if (nz > 2u) {
+        constexpr int JP = V * NV;
+        const float* row = p.table + (uint64_t)id * JP;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          float x[V];
+          ld_row<V>(row + i * V, pol_tab, x);
+#pragma unroll
+          for (int c = 0; c < V; ++c) sum += clamp_fast((double)x[c], s_r1[i * V + c], s_l1[i * V + c]);
+        }
+      }
+    }
+    if (nz <= 2u) {
+      // absent columns hold loss 0: clamp(0; R >= 0, L) = +0 exactly, so n < 2 needs no branch
+      sum += clamp_fast((double)__uint_as_float(r.y), s_r1[c1], s_l1[c1]);  // steps 1-2: FT1, sum over ELTs
+      sum += clamp_fast((double)__uint_as_float(r.z), s_r1[c2], s_l1[c2]);
+    }
+    return clamp_fast(sum, p.r2, p.l2);  // step 3: FT2 (exactly +0 for an empty record)
+  }
+};
+
+template <int V, int NV, int G, bool kRec>
+struct BatchOf {
+  using type = RowBatch<V, NV, G>;
+};
+template <int V, int NV>
+struct BatchOf<V, NV, 1, true> {
+  using type = RecBatch<V, NV>;
+};
+
 // Per-warp bookkeeping of the (at most two) trials whose hits are still in flight (carried queue).
 struct WarpTrials {
   uint64_t trial[2];  // trial index per parity slot
@@ -143,8 +197,8 @@ template <int V, int NV, int G, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_constant__ LayerParams p) {
   constexpr int JP = V * NV;
   constexpr unsigned FULL = 0xffffffffu;
-  using Batch = RowBatch<V, NV, G>;
-  constexpr bool kCarry = (G == 1) && Batch::kAsync;
+  constexpr bool kCarry = (G == 1) && RowBatch<V, NV, G>::kAsync;  // narrow rows: records + carried queue
+  using Batch = typename BatchOf<V, NV, G, kCarry>::type;
   extern __shared__ uint32_t smem[];
   // FT1 terms, padded to the G*NVL*V columns a row group covers (padding: R = 0, L = +inf, so the
   // branch-free FT1 of a padding column -- always loss 0 -- is exactly +0).
@@ -216,7 +270,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   auto consume = [&]() {
     if (bn != 0) {
       if constexpr (kCarry) {
-        const double o = rows.row_loss(p, s_r1, s_l1);
+        const double o = rows.row_loss(p, s_r1, s_l1, pol_tab);
         const bool mine = lane < bn;
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
@@ -229,7 +283,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
           }
         }
       } else {
-        rows.consume(p, lane, s_r1, s_l1, S0);
+        if constexpr (!kCarry) rows.consume(p, lane, s_r1, s_l1, S0);
       }
       bn = 0;
     }
@@ -241,7 +295,11 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     __syncwarp();
     const uint32_t word = lane < n ? q[(head + lane) & (kQueue - 1)] : 0u;
     btag = word >> 31;
-    rows.issue(p, q, head, n, lane, pol_tab, s_r1, s_l1, S0);
+    if constexpr (kCarry) {
+      rows.issue(p, q, head, n, lane, pol_tab);
+    } else {
+      rows.issue(p, q, head, n, lane, pol_tab, s_r1, s_l1, S0);
+    }
     __syncwarp();
     bstart = issued;
     bn = n;
