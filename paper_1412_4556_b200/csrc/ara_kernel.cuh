@@ -46,6 +46,7 @@ struct LayerParams {
   uint32_t fold_words;       // bitmap words held in shared memory (<= present_words; folded mod fold_words)
   uint64_t fold_magic;       // floor((2^64 - 1) / fold_words) + 1: fast word % fold_words (Lemire)
   const uint4* rec;          // per-event sparse row record (presence kernel, rows <= 16 columns)
+  uint32_t pf_dist;          // presence kernel: L2 prefetch distance in windows (0 = off)
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
 
@@ -134,6 +135,8 @@ __device__ __forceinline__ void st_shared_if(uint32_t* ptr, uint32_t v, bool pre
   asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.shared.u32 [%0], %1;\n}"
                :: "r"((uint32_t)__cvta_generic_to_shared(ptr)), "r"(v), "r"((int)pred) : "memory");
 }
+
+__device__ __forceinline__ void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr)); }
 
 // V: floats per vector load; NV: vectors per row (jpad = V*NV); G: lanes per row (power of 2 <= 32);
 // U: rows per row group per iteration.

@@ -360,17 +360,33 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       }
       return v;
     };
-    uint4 cur = load4(0);
-    uint4 nx1 = load4(128);
-    for (uint32_t rel = 0; rel < len; rel += 128) {
-      const uint4 nx2 = load4(rel + 256);
+    // Full windows (16-B aligned trial, 128 ids inside the trial) stream through a running per-lane
+    // pointer with no bounds checks; the trial's last partial window (or an unaligned trial) goes
+    // through the checked loader.  One window is held ahead in registers; optionally lanes 0-3 also
+    // prefetch the window pf_dist ahead into L2.
+    const uint32_t nwin = (len + 127) / 128;
+    const uint32_t nfull = vec ? len / 128 : 0u;
+    const uint4* lp = reinterpret_cast<const uint4*>(base) + lane;
+    const uint32_t pfd = p.pf_dist;
+    auto load_win = [&](uint32_t w) -> uint4 {
+      if (w < nfull) return ld_ids4(reinterpret_cast<const uint32_t*>(lp + (size_t)w * 32), pol_yet);
+      if (w < nwin) return load4(w * 128);
+      return make_uint4(0u, 0u, 0u, 0u);
+    };
+    uint32_t mxv = 0u, mnv = 0xffffffffu;  // extremes of the ids of the full windows
+    uint4 cur = load_win(0);
+    for (uint32_t w = 0; w < nwin; ++w) {
+      const uint4 nxt = load_win(w + 1);
+      if (pfd && lane < 4) {
+        const uint32_t at = (w + pfd) * 128 + 32u * lane;
+        if (at < len) prefetch_l2(base + at);
+      }
       const uint32_t id[4] = {cur.x, cur.y, cur.z, cur.w};
-      // validity: every id of the window in [1, C] (positions past the end hold 0 and are excused)
-      if (rel + 128 <= len) {
-        const uint32_t mn = min(min(id[0], id[1]), min(id[2], id[3]));
-        const uint32_t mx = max(max(id[0], id[1]), max(id[2], id[3]));
-        bad |= (mn == 0u || mx > C) ? 1u : 0u;
-      } else {
+      if (w < nfull) {  // validity is checked once per trial from the running extremes
+        mxv = max(mxv, max(max(id[0], id[1]), max(id[2], id[3])));
+        mnv = min(mnv, min(min(id[0], id[1]), min(id[2], id[3])));
+      } else {  // checked window: positions past the end read 0 and are excused
+        const uint32_t rel = w * 128;
 #pragma unroll
         for (int u = 0; u < 4; ++u) bad |= (rel + 4u * lane + u < len && id[u] - 1u >= C) ? 1u : 0u;
       }
@@ -381,20 +397,28 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
         wd = fold_small ? min(wd, wd - fw) : (uint32_t)__umul64hi(fmagic * (uint64_t)wd, (uint64_t)fw);
         hit[u] = (bits[wd] >> (id[u] & 31u)) & 1u;  // id 0 -> bit 0 of word 0, never set
       }
+      // Append the hits in a fixed order that depends only on the window: per pair of slots, first the
+      // lanes' first hit of the pair (lanes ascending), then -- only if some lane hit both -- the
+      // second ids of those lanes.  One ballot per pair instead of one per slot.
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const unsigned m0 = __ballot_sync(FULL, hit[2 * h]);
-        const unsigned m1 = __ballot_sync(FULL, hit[2 * h + 1]);
-        const unsigned n0 = __popc(m0);
-        const unsigned at = head + count;
-        st_shared_if(q + ((at + __popc(m0 & lt)) & (kQueue - 1)), tag | id[2 * h], hit[2 * h]);
-        st_shared_if(q + ((at + n0 + __popc(m1 & lt)) & (kQueue - 1)), tag | id[2 * h + 1], hit[2 * h + 1]);
-        count += n0 + __popc(m1);
+        const bool ha = hit[2 * h], hb = hit[2 * h + 1];
+        const bool any = ha || hb;
+        const uint32_t first = tag | (ha ? id[2 * h] : id[2 * h + 1]);
+        const unsigned m = __ballot_sync(FULL, any);
+        st_shared_if(q + ((head + count + __popc(m & lt)) & (kQueue - 1)), first, any);
+        count += __popc(m);
+        const bool both = ha && hb;
+        if (__any_sync(FULL, both)) {  // rare: ~1% of lanes per pair
+          const unsigned m2 = __ballot_sync(FULL, both);
+          st_shared_if(q + ((head + count + __popc(m2 & lt)) & (kQueue - 1)), tag | id[2 * h + 1], both);
+          count += __popc(m2);
+        }
         while (count >= 32) issue(32);  // warp-uniform; at most 31 + 64 = 95 < kQueue queued
       }
-      cur = nx1;
-      nx1 = nx2;
+      cur = nxt;
     }
+    if (nfull) bad |= (mnv == 0u || mxv > C) ? 1u : 0u;
     __syncwarp();
     if (lane == 0) {
       wt.end[par] = issued + count;
