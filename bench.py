@@ -38,7 +38,7 @@ UNIT = "ms/1M-trial run"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="P")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -78,7 +78,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                          "-lms", "20", "-i", str(self.index)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -409,7 +409,9 @@ def main():
     lookups_exact = float(sum(len(l.elts) for l in cfg.layers)) * (
         N * cfg.kmin if cfg.fixed_length else float(synth.trial_offsets(cfg.seed, N, cfg.kmin, cfg.kmax)[-1]))
     value = ms_per_step * 1e6 / N
-    n_metric_launches = L * 9 * ((len(rps) + 15) // 16) if rps else 0
+    # one ara_layer/presence launch per layer, one fused (cooperative) metric launch per layer and batch
+    # of <= 16 return periods; the NCCL all-gather (N > 1) and ara_unshard's memcpy2D are not our kernels
+    n_metric_launches = L * ((len(rps) + 15) // 16) if rps else 0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,

@@ -109,6 +109,15 @@ def yet_ids(seed: int, catalog_size: int, q0: int, count: int) -> np.ndarray:
     return (uni_np(r, catalog_size) + np.uint64(1)).astype(np.uint32)
 
 
+def yet_ids_chunked(seed: int, catalog_size: int, q0: int, count: int, chunk: int = 1 << 26) -> np.ndarray:
+    """Same as yet_ids, generated in chunks (bounded host memory for multi-GB YETs)."""
+    out = np.empty(count, dtype=np.uint32)
+    for a in range(0, count, chunk):
+        b = min(count, a + chunk)
+        out[a:b] = yet_ids(seed, catalog_size, q0 + a, b - a)
+    return out
+
+
 def trial_lengths(seed: int, t0: int, count: int, kmin: int, kmax: int) -> np.ndarray:
     if kmin == kmax:
         return np.full(count, kmin, dtype=np.uint64)
@@ -273,7 +282,7 @@ def make_yet(cfg: Config, t0: int = 0, t1: Optional[int] = None) -> YetData:
     n = t1 - t0
     if cfg.fixed_length:
         k = cfg.kmin
-        ids = yet_ids(cfg.seed, cfg.catalog_size, t0 * k, n * k)
+        ids = yet_ids_chunked(cfg.seed, cfg.catalog_size, t0 * k, n * k)
         return YetData(ids, None, n, k)
     off = trial_offsets(cfg.seed, cfg.num_trials, cfg.kmin, cfg.kmax)
     q0, q1 = int(off[t0]), int(off[t1])
