@@ -138,6 +138,21 @@ __device__ __forceinline__ void st_shared_if(uint32_t* ptr, uint32_t v, bool pre
 
 __device__ __forceinline__ void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr)); }
 
+// Warp-synchronous primitives as inline PTX for full-warp, converged call sites (the presence kernel's
+// scan): avoids the divergence-handling slow paths nvcc wraps around the intrinsics.
+__device__ __forceinline__ unsigned ballot_full(bool p) {
+  unsigned r;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n vote.sync.ballot.b32 %0, q, 0xffffffff;\n}"
+               : "=r"(r) : "r"((unsigned)p));
+  return r;
+}
+__device__ __forceinline__ bool any_full(bool p) {
+  unsigned r;
+  asm volatile("{\n .reg .pred q, o;\n setp.ne.u32 q, %1, 0;\n vote.sync.any.pred o, q, 0xffffffff;\n selp.u32 %0, 1, 0, o;\n}"
+               : "=r"(r) : "r"((unsigned)p));
+  return r != 0;
+}
+
 // V: floats per vector load; NV: vectors per row (jpad = V*NV); G: lanes per row (power of 2 <= 32);
 // U: rows per row group per iteration.
 template <int V, int NV, int G, int U>
