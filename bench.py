@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--sweep", action="store_true", help="launch-shape sweep (E8); extra JSON lines to stderr")
     ap.add_argument("--cpu-sample", type=int, default=65536, help="trials in the cpu_baseline sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cold/cpu legs")
+    ap.add_argument("--study", action="store_true",
+                    help="Section IV.B data-structure study (interleaved / independent / sorted ELTs); JSON lines to stderr")
     return ap.parse_args()
 
 
@@ -441,8 +443,42 @@ def main():
 
     if args.sweep:
         sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ)
+    if args.study:
+        study(ctx, cfg, ids, offsets_d, offsets_h, K, n_local, L, ylt_local, stream, occ, kern_ms)
     if world > 1:
         dist.destroy_process_group()
+
+
+def study(ctx, cfg, ids, offsets_d, offsets_h, K, n_local, L, ylt_local, stream, occ, kern_ms):
+    """PAPER.md:209-213 (Section IV.B): the same Algorithm 1 over three ELT representations.  Each layout
+    runs a plain one-lane-per-occurrence kernel; the product kernels are listed beside for reference.
+    The sorted/binary-search layout runs on a 1/16 trial subset and is scaled."""
+    import torch
+
+    from paper_1412_4556_b200 import ara
+    J = sum(len(l.elts) for l in cfg.layers) / L
+    for layout, name in ((ara.STUDY_INTERLEAVED, "interleaved"), (ara.STUDY_INDEPENDENT, "independent"),
+                         (ara.STUDY_SORTED, "sorted+binary-search")):
+        n = n_local if layout != ara.STUDY_SORTED else max(1, n_local // 16)
+        if offsets_d is None:
+            sub_ids, sub_off = ids[: n * K], None
+        else:
+            sub_ids, sub_off = ids, offsets_d[: n + 1]
+        ctx.ara_run_study(layout, sub_ids, ylt_local, offsets=sub_off, events_per_trial=K, num_trials=n, stream=stream)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        a.record(stream)
+        for _ in range(reps):
+            ctx.ara_run_study(layout, sub_ids, ylt_local, offsets=sub_off, events_per_trial=K, num_trials=n, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps * (n_local / n)
+        print(json.dumps({"study": name, "ms_per_1M_trial_run": ms * 1e6 / n_local / 1.0,
+                          "launch_ms_all_layers": ms, "lookups_per_s": occ * J * L / (ms * 1e-3),
+                          "subset_trials": n}), file=sys.stderr, flush=True)
+    print(json.dumps({"study": "product (presence/dense, ara_run)", "launch_ms_all_layers": kern_ms,
+                      "lookups_per_s": occ * J * L / (kern_ms * 1e-3)}), file=sys.stderr, flush=True)
 
 
 def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):

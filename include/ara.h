@@ -142,6 +142,18 @@ ARA_API ara_status ara_pml_tvar(const double* ylt, uint64_t n, const double* rps
 ARA_API ara_status ara_pml(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream);
 ARA_API ara_status ara_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream);
 
+/* Section IV.B data-structure study: Algorithm 1 with the same plain kernel (one
+ * warp per trial, one lane per occurrence) over one of three ELT representations, for comparing their
+ * memory behaviour on B200 -- not the product path:
+ *   0 ARA_STUDY_INTERLEAVED  the combined event-major table (one row per event)
+ *   1 ARA_STUDY_INDEPENDENT  one direct-access array per ELT (the paper's GPU choice)
+ *   2 ARA_STUDY_SORTED       per-ELT arrays sorted by event id, binary search
+ * The extra structures are built on first use (layout 2 copies the table to the host once).  Same
+ * YET / YLT conventions as ara_run; asynchronous except for that first build.  Invalid ids read as
+ * absent and are not reported. */
+typedef enum { ARA_STUDY_INTERLEAVED = 0, ARA_STUDY_INDEPENDENT = 1, ARA_STUDY_SORTED = 2 } ara_study_layout;
+ARA_API ara_status ara_run_study(ara_ctx* ctx, int layout, const ara_yet* yet, double* ylt, void* stream);
+
 /* Host-only memory accounting of one layer's direct-access table: bytes of the
  * (C+1)-row table and its row stride.  No device needed. */
 ARA_API ara_status ara_table_footprint(uint32_t catalog_size, uint32_t num_elts, uint64_t* bytes, uint32_t* row_stride);

@@ -24,10 +24,11 @@ ARA_OK, ARA_E_ARG, ARA_E_RANGE, ARA_E_DUP, ARA_E_VALUE, ARA_E_NOMEM, ARA_E_CUDA,
 ARA_OPT_BLOCK_THREADS, ARA_OPT_BLOCKS_PER_SM, ARA_OPT_L2_POLICY, ARA_OPT_VARIANT, ARA_OPT_KERNEL = 1, 2, 3, 4, 5
 ARA_OPT_PREFETCH = 6
 KERNEL_AUTO, KERNEL_PRESENCE, KERNEL_DENSE = -1, 0, 1
+STUDY_INTERLEAVED, STUDY_INDEPENDENT, STUDY_SORTED = 0, 1, 2
 ARA_MAX_ELTS_PER_LAYER = 128
 
 #: every symbol include/ara.h declares (checked by tests/test_abi.py against the header and the .so)
-EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_host", "ara_check", "ara_pml_tvar", "ara_pml",
+EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_host", "ara_run_study", "ara_check", "ara_pml_tvar", "ara_pml",
            "ara_tvar", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
            "ara_layer_info", "ara_layer_stats", "ara_table_row", "ara_status_string", "ara_last_error", "ara_version")
 
@@ -74,6 +75,7 @@ def lib() -> ctypes.CDLL:
             "ara_destroy": (None, [vp]),
             "ara_run": (st, [vp, ctypes.POINTER(_Yet), dp, vp]),
             "ara_run_host": (st, [vp, ctypes.POINTER(_Yet), dp, vp]),
+            "ara_run_study": (st, [vp, ctypes.c_int, ctypes.POINTER(_Yet), dp, vp]),
             "ara_check": (st, [vp, vp]),
             "ara_pml_tvar": (st, [dp, u64, dp, u32, dp, dp, vp]),
             "ara_pml": (st, [dp, u64, dp, u32, dp, vp]),
@@ -227,6 +229,14 @@ class Context:
                                                        _numel(event_ids) // max(1, events_per_trial))
         y = _yet_struct(event_ids, offsets, n, events_per_trial)
         _check(lib().ara_run_host(self._h, ctypes.byref(y), _dptr(ylt_host), _stream_ptr(stream)), "ara_run_host")
+
+    def ara_run_study(self, layout: int, event_ids, ylt, offsets=None, events_per_trial: int = 0,
+                      num_trials: Optional[int] = None, stream=None) -> None:
+        """Section IV.B data-structure study kernel (device YET -> device YLT)."""
+        n = num_trials if num_trials is not None else (offsets.numel() - 1 if offsets is not None else
+                                                       event_ids.numel() // max(1, events_per_trial))
+        y = _yet_struct(event_ids, offsets, n, events_per_trial)
+        _check(lib().ara_run_study(self._h, layout, ctypes.byref(y), _dptr(ylt), _stream_ptr(stream)), "ara_run_study")
 
     def ara_check(self, stream=None) -> None:
         _check(lib().ara_check(self._h, _stream_ptr(stream)), "ara_check")

@@ -16,6 +16,7 @@
 #include "ara_kernel.cuh"
 #include "presence_kernel.cuh"
 #include "variants.cuh"
+#include "study.cuh"
 #include "common.cuh"
 
 namespace ara {
@@ -61,6 +62,11 @@ struct Layer {
   uint64_t table_bytes = 0;
   uint32_t* present = nullptr;  // presence bitmap, (C + 1 + 31) / 32 words
   uint4* rec = nullptr;         // sparse row records (C + 1) x 16 B, rows of <= 16 columns
+  // Section IV.B study structures, built on first use by ara_run_study
+  float* indep = nullptr;         // J x (C + 1) independent per-ELT direct-access arrays
+  uint32_t* sorted_ids = nullptr; // per-ELT (event, loss) pairs sorted by event
+  float* sorted_loss = nullptr;
+  uint32_t* sorted_off = nullptr; // J + 1
   uint32_t present_words = 0;
   std::vector<const Variant*> variants[2];  // by KernelKind
   uint64_t present_rows = 0;                // rows holding at least one loss
@@ -200,6 +206,10 @@ static void destroy_ctx(ara_ctx* c) {
     cudaFree(L.table);
     cudaFree(L.present);
     cudaFree(L.rec);
+    cudaFree(L.indep);
+    cudaFree(L.sorted_ids);
+    cudaFree(L.sorted_loss);
+    cudaFree(L.sorted_off);
   }
   cudaFree(c->d_err);
   cudaFreeHost(c->h_err);
@@ -604,6 +614,85 @@ ara_status ara_run_host(ara_ctx* c, const ara_yet* yet, double* ylt_host, void* 
     ++b;
   }
   return take_err(c, s);
+}
+
+ara_status ara_run_study(ara_ctx* c, int layout, const ara_yet* yet, double* ylt, void* stream) {
+  if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
+  if (layout < STUDY_INTERLEAVED || layout > STUDY_SORTED) return set_error(ARA_E_ARG, "unknown layout %d", layout);
+  ara_status st = check_yet(yet);
+  if (st) return st;
+  if (yet->num_trials == 0) return ARA_OK;
+  if (!ylt) return set_error(ARA_E_ARG, "ylt is NULL");
+  DeviceGuard guard(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t rows = (uint64_t)c->C + 1;
+  for (size_t l = 0; l < c->layers.size(); ++l) {
+    Layer& L = c->layers[l];
+    if (layout == STUDY_INDEPENDENT && !L.indep) {
+      if (cudaMalloc(&L.indep, rows * L.J * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(ARA_E_NOMEM, "independent tables");
+      }
+      study_transpose(L.indep, L.table, L.jpad, L.J, rows, c->sms, s);
+      ARA_CUDA(cudaGetLastError());
+    }
+    if (layout == STUDY_SORTED && !L.sorted_ids) {
+      std::vector<float> h(rows * L.jpad);
+      ARA_CUDA(cudaStreamSynchronize(s));
+      ARA_CUDA(cudaMemcpy(h.data(), L.table, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+      std::vector<uint32_t> off(L.J + 1, 0), ids;
+      std::vector<float> loss;
+      for (uint32_t j = 0; j < L.J; ++j) {
+        for (uint64_t e = 1; e < rows; ++e)
+          if (h[e * L.jpad + j] != 0.0f) {
+            ids.push_back((uint32_t)e);
+            loss.push_back(h[e * L.jpad + j]);
+          }
+        off[j + 1] = (uint32_t)ids.size();
+      }
+      const size_t n = std::max<size_t>(1, ids.size());
+      if (cudaMalloc(&L.sorted_ids, n * 4) != cudaSuccess || cudaMalloc(&L.sorted_loss, n * 4) != cudaSuccess ||
+          cudaMalloc(&L.sorted_off, off.size() * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(ARA_E_NOMEM, "sorted ELT arrays");
+      }
+      ARA_CUDA(cudaMemcpy(L.sorted_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
+      ARA_CUDA(cudaMemcpy(L.sorted_loss, loss.data(), loss.size() * 4, cudaMemcpyHostToDevice));
+      ARA_CUDA(cudaMemcpy(L.sorted_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+    }
+    StudyParams p;
+    memset(&p, 0, sizeof p);
+    p.table = L.table;
+    p.indep = L.indep;
+    p.sorted_ids = L.sorted_ids;
+    p.sorted_loss = L.sorted_loss;
+    p.sorted_off = L.sorted_off;
+    p.ids = yet->event_ids;
+    p.offsets = yet->trial_offsets;
+    p.num_trials = yet->num_trials;
+    p.rows = rows;
+    p.K = yet->events_per_trial;
+    p.C = c->C;
+    p.J = L.J;
+    p.jpad = L.jpad;
+    p.ylt = ylt + l * yet->num_trials;
+    p.r2 = L.r2;
+    p.l2 = L.l2;
+    p.r3 = L.r3;
+    p.l3 = L.l3;
+    for (int j = 0; j < kMaxJ; ++j) {
+      p.r1[j] = L.r1[j];
+      p.l1[j] = L.l1[j];
+    }
+    void* fn = study_kernel_fn(layout);
+    int bps = 0;
+    ARA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, 256, 0));
+    uint64_t blocks = (uint64_t)c->sms * std::max(1, bps);
+    blocks = std::min<uint64_t>(blocks, (yet->num_trials + 7) / 8);
+    void* args[] = {&p};
+    ARA_CUDA(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(256), args, 0, s));
+  }
+  return ARA_OK;
 }
 
 ara_status ara_unshard(const double* gathered, uint32_t G, uint64_t cap, uint32_t L, const uint64_t* starts,

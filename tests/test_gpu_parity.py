@@ -385,3 +385,27 @@ def test_metrics_fused_and_pass_kernels_agree(cuda_device, monkeypatch):
         monkeypatch.delenv("ARA_METRICS_PASSES")
         assert np.array_equal(p1, p2) and np.array_equal(p1, oracle.pml(y, rps)), n
         assert np.array_equal(t1, oracle.tvar(y, rps)) and np.array_equal(t2, t1), n
+
+
+@pytest.mark.parametrize("layout", [ara.STUDY_INTERLEAVED, ara.STUDY_INDEPENDENT, ara.STUDY_SORTED])
+def test_section_4b_study_layouts(cuda_device, layout):
+    """The Section IV.B data-structure study kernels compute the same YLT."""
+    for J, kw in ((16, {}), (3, {}), (24, dict(seed=5))):
+        C, elts, layer, yet, N, K = _small_problem(J, **kw)
+        want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+        ctx = _ctx_from(C, elts, [layer])
+        ids = torch.from_numpy(yet.view(np.int32)).cuda()
+        out = torch.full((1, N), -1.0, dtype=torch.float64, device=cuda_device)
+        ctx.ara_run_study(layout, ids, out, events_per_trial=K, num_trials=N)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), want), (layout, J)
+    cfg = synth.Config.load("V")  # variable-length trials, real regime
+    elts = synth.make_elts(cfg)
+    y = synth.make_yet(cfg, 0, 500)
+    want = oracle.ylt_for(cfg, elts, y)
+    ctx = ara.context_for_config(cfg, elts)
+    out = torch.zeros((1, 500), dtype=torch.float64, device=cuda_device)
+    ctx.ara_run_study(layout, torch.from_numpy(y.event_ids.view(np.int32)).cuda(), out,
+                      offsets=torch.from_numpy(y.offsets.view(np.int64)).cuda())
+    torch.cuda.synchronize()
+    assert np.all(within_tol(out.cpu().numpy(), want))
