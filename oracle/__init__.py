@@ -59,6 +59,12 @@ def _L():
                                    ctypes.c_uint32, ctypes.POINTER(_Elt), ctypes.c_uint32,
                                    ctypes.POINTER(_Layer), ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_void_p]
+        lib.oracle_ylt_olt.restype = ctypes.c_int
+        lib.oracle_ylt_olt.argtypes = lib.oracle_ylt.argtypes + [ctypes.c_void_p]
+        lib.oracle_aal.restype = ctypes.c_double
+        lib.oracle_aal.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+        lib.oracle_ep.restype = None
+        lib.oracle_ep.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]
         lib.oracle_trial_detail.restype = ctypes.c_int
         lib.oracle_trial_detail.argtypes = [ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint64,
                                             ctypes.POINTER(_Elt), ctypes.c_uint32, ctypes.POINTER(_Layer),
@@ -122,6 +128,34 @@ def ylt(catalog_size: int, yet_ids: np.ndarray, offsets: Optional[np.ndarray], n
     if rc:
         raise OracleError(f"oracle_ylt failed with code {rc}")
     return out
+
+
+def ylt_olt(catalog_size: int, yet_ids: np.ndarray, offsets: Optional[np.ndarray], num_trials: int,
+            events_per_trial: int, elts, layers, lookup: int = LOOKUP_BINARY, threads: int = 0):
+    """(YLT, OLT): OLT[l][t] = largest occurrence-net loss of trial t under layer l."""
+    yet_ids = np.ascontiguousarray(yet_ids, dtype=np.uint32)
+    off = None if offsets is None else np.ascontiguousarray(offsets, dtype=np.uint64)
+    ce, cl, keep = _marshal(elts, layers)
+    y = np.zeros((len(layers), num_trials), dtype=np.float64)
+    o = np.zeros((len(layers), num_trials), dtype=np.float64)
+    rc = _L().oracle_ylt_olt(catalog_size, _ptr(yet_ids), 0 if off is None else _ptr(off), num_trials,
+                             events_per_trial, ce, len(elts), cl, len(layers), lookup, threads, _ptr(y), _ptr(o))
+    if rc:
+        raise OracleError(f"oracle_ylt_olt failed with code {rc}")
+    return y, o
+
+
+def aal(y: np.ndarray) -> float:
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return _L().oracle_aal(_ptr(y), y.size)
+
+
+def ep(y: np.ndarray, thresholds: Sequence[float]) -> np.ndarray:
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    x = np.ascontiguousarray(thresholds, dtype=np.float64)
+    out = np.zeros(max(1, x.size))
+    _L().oracle_ep(_ptr(y), y.size, _ptr(x), x.size, _ptr(out))
+    return out[:x.size]
 
 
 def trial_detail(catalog_size: int, ids: Sequence[int], elts, layer, lookup: int = LOOKUP_BINARY):

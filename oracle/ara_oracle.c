@@ -106,6 +106,7 @@ typedef struct {
   int mode;
   uint64_t t_lo, t_hi;
   double* ylt; /* this layer's row */
+  double* olt; /* this layer's occurrence-loss row, or NULL */
 } work_t;
 
 static void* run_block(void* arg) {
@@ -114,8 +115,14 @@ static void* run_block(void* arg) {
     uint64_t b = w->offsets ? w->offsets[t] : t * (uint64_t)w->K;
     uint64_t e = w->offsets ? w->offsets[t + 1] : b + w->K;
     double S = 0.0; /* step 4: cumulative sum of occurrence-net losses, event (time) order */
-    for (uint64_t k = b; k < e; ++k) S = S + occurrence_loss(w->ids[k], w->tabs, w->elts, w->layer, w->mode);
+    double M = 0.0; /* largest occurrence-net loss of the trial */
+    for (uint64_t k = b; k < e; ++k) {
+      double o = occurrence_loss(w->ids[k], w->tabs, w->elts, w->layer, w->mode);
+      S = S + o;
+      if (o > M) M = o;
+    }
     w->ylt[t] = oracle_clamp(S, w->layer->ft3_retention, w->layer->ft3_limit); /* FT3 */
+    if (w->olt) w->olt[t] = M;
   }
   return NULL;
 }
@@ -140,6 +147,13 @@ static int check_inputs(uint32_t C, const oracle_elt* elts, uint32_t num_elts, c
 int oracle_ylt(uint32_t catalog_size, const uint32_t* yet_ids, const uint64_t* offsets, uint64_t num_trials,
                uint32_t events_per_trial, const oracle_elt* elts, uint32_t num_elts, const oracle_layer* layers,
                uint32_t num_layers, int lookup_mode, int threads, double* ylt) {
+  return oracle_ylt_olt(catalog_size, yet_ids, offsets, num_trials, events_per_trial, elts, num_elts, layers,
+                        num_layers, lookup_mode, threads, ylt, NULL);
+}
+
+int oracle_ylt_olt(uint32_t catalog_size, const uint32_t* yet_ids, const uint64_t* offsets, uint64_t num_trials,
+                   uint32_t events_per_trial, const oracle_elt* elts, uint32_t num_elts, const oracle_layer* layers,
+                   uint32_t num_layers, int lookup_mode, int threads, double* ylt, double* olt) {
   int rc = check_inputs(catalog_size, elts, num_elts, layers, num_layers);
   if (rc) return rc;
   uint64_t total = offsets ? offsets[num_trials] - offsets[0] : num_trials * (uint64_t)events_per_trial;
@@ -168,7 +182,7 @@ int oracle_ylt(uint32_t catalog_size, const uint32_t* yet_ids, const uint64_t* o
     for (int i = 0; i < threads; ++i) {
       w[i] = (work_t){catalog_size, yet_ids, offsets, events_per_trial, tabs, elts, &layers[l], lookup_mode,
                       num_trials * (uint64_t)i / threads, num_trials * (uint64_t)(i + 1) / threads,
-                      ylt + (uint64_t)l * num_trials};
+                      ylt + (uint64_t)l * num_trials, olt ? olt + (uint64_t)l * num_trials : NULL};
       if (threads == 1)
         run_block(&w[i]);
       else
@@ -266,4 +280,19 @@ int oracle_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, do
   }
   free(c);
   return ORACLE_OK;
+}
+
+double oracle_aal(const double* ylt, uint64_t n) {
+  double s = 0.0;
+  for (uint64_t t = 0; t < n; ++t) s = s + ylt[t];
+  return n ? s / (double)n : 0.0;
+}
+
+void oracle_ep(const double* ylt, uint64_t n, const double* x, uint32_t m, double* out) {
+  for (uint32_t i = 0; i < m; ++i) {
+    uint64_t c = 0;
+    for (uint64_t t = 0; t < n; ++t)
+      if (ylt[t] >= x[i]) ++c;
+    out[i] = n ? (double)c / (double)n : 0.0;
+  }
 }

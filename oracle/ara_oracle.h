@@ -63,6 +63,19 @@ int oracle_ylt(uint32_t catalog_size, const uint32_t* yet_ids, const uint64_t* o
                uint32_t events_per_trial, const oracle_elt* elts, uint32_t num_elts, const oracle_layer* layers,
                uint32_t num_layers, int lookup_mode, int threads, double* ylt);
 
+/* Same as oracle_ylt, also writing olt[l][t] = the largest occurrence-net loss o of trial t under
+ * layer l (0 for an empty trial): the occurrence-basis loss table behind OEP metrics (
+ * SPEC.md:460 names the occurrence basis).  olt may be NULL. */
+int oracle_ylt_olt(uint32_t catalog_size, const uint32_t* yet_ids, const uint64_t* offsets, uint64_t num_trials,
+                   uint32_t events_per_trial, const oracle_elt* elts, uint32_t num_elts, const oracle_layer* layers,
+                   uint32_t num_layers, int lookup_mode, int threads, double* ylt, double* olt);
+
+/* Average annual loss: the mean of the YLT, summed in trial order ("AAL"). */
+double oracle_aal(const double* ylt, uint64_t n);
+
+/* Exceedance probability at m thresholds: #{t : ylt[t] >= x} / n (SPEC.md:402-408 exceedance_curve). */
+void oracle_ep(const double* ylt, uint64_t n, const double* x, uint32_t m, double* out);
+
 /* One trial, one layer, event by event: o[k] occurrence-net loss, S[k] prefix sum, a[k] =
  * F3(S_k) - F3(S_{k-1}) per-event aggregate-net loss (SPEC.md "incremental erosion").  Returns the
  * trial loss F3(S_n) through *ylt. */

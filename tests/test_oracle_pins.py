@@ -304,3 +304,32 @@ def test_metric_invariants():
     assert np.allclose(oracle.tvar(dup, rps), t, rtol=1e-15, atol=0)
     c = np.full(50, 7.5)
     assert np.all(oracle.pml(c, [2.0, 50.0]) == 7.5) and np.all(oracle.tvar(c, [2.0, 50.0]) == 7.5)
+
+
+# ------------------------------------------------------------------ N4 outputs: OLT (occurrence basis), AAL, EP
+def test_olt_extended_example():
+    g = golden("extended_example.json")
+    trials = g["trials"]
+    ids = np.array([e for t in trials for e in t], dtype=np.uint32)
+    off = np.zeros(len(trials) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(t) for t in trials])
+    y, o = oracle.ylt_olt(g["catalog_size"], ids, off, len(trials), 0, golden_elts(g), [golden_layer(g)])
+    assert list(y[0]) == g["ylt"] and list(o[0]) == g["olt"]
+
+
+def test_olt_bounds_and_relation_to_ylt():
+    C, elts, layer, yet, N, K = _rand_problem(11)
+    y, o = oracle.ylt_olt(C, yet, None, N, K, elts, [layer])
+    assert np.all(o >= 0) and np.all(o <= layer[1][1])           # occurrence losses are within FT2's limit
+    ident = (layer[0], layer[1], (0.0, INF))
+    s, _ = oracle.ylt_olt(C, yet, None, N, K, elts, [ident])
+    assert np.all(o <= s)                                          # the largest occurrence <= the trial sum
+    assert np.array_equal(y, oracle.ylt(C, yet, None, N, K, elts, [layer]))
+
+
+def test_aal_and_ep_examples():
+    g = golden("metrics_examples.json")
+    assert oracle.aal(np.arange(1, 11.0)) == g["aal_1to10"]
+    assert list(oracle.ep(np.array(g["ep_losses"]), g["ep_thresholds"])) == g["ep_probs"]
+    y = np.array([0.0, 5.0, 5.0, 7.0])
+    assert oracle.aal(y) == 4.25 and list(oracle.ep(y, [5.0, 5.1, 0.0])) == [0.75, 0.25, 1.0]
