@@ -119,6 +119,12 @@ ARA_API void ara_destroy(ara_ctx* ctx); /* NULL is a no-op; synchronises the dev
  * Errors (immediate): ARA_E_ARG (NULL, num_events too small for fixed-length trials), ARA_E_CUDA. */
 ARA_API ara_status ara_run(ara_ctx* ctx, const ara_yet* yet, double* ylt, void* stream);
 
+/* ara_run plus the occurrence-basis loss table: olt[l * num_trials + t] = the largest occurrence-net
+ * loss (FT2 output) over trial t's events under layer l, 0 for a trial without events (DEVICE,
+ * caller-allocated like ylt; NULL = not produced).  PML/TVaR of an OLT row are OEP-basis metrics
+ * (SURVEY.md N4).  Same conventions and errors as ara_run. */
+ARA_API ara_status ara_run_ex(ara_ctx* ctx, const ara_yet* yet, double* ylt, double* olt, void* stream);
+
 /* End-to-end variant for a HOST YET (pinned memory gives copy/compute overlap; pageable works but
  * serialises): the YET is streamed to the device in trial batches on an internal copy stream,
  * overlapped with the analysis of the previous batch, and the YLT is written to HOST ylt_host
@@ -153,6 +159,23 @@ ARA_API ara_status ara_tvar(const double* ylt, uint64_t n, const double* rps, ui
  * absent and are not reported. */
 typedef enum { ARA_STUDY_INTERLEAVED = 0, ARA_STUDY_INDEPENDENT = 1, ARA_STUDY_SORTED = 2 } ara_study_layout;
 ARA_API ara_status ara_run_study(ara_ctx* ctx, int layout, const ara_yet* yet, double* ylt, void* stream);
+
+/* Average annual loss of a DEVICE YLT of n values: the mean, reduced in a fixed order (bitwise
+ * reproducible).  Result to HOST *out; synchronises `stream`.  ARA_E_ARG for NULL / n == 0. */
+ARA_API ara_status ara_aal(const double* ylt, uint64_t n, double* out, void* stream);
+
+/* Exceedance probabilities of a DEVICE YLT at m HOST thresholds: out[i] = #{t : ylt[t] >= x[i]} / n
+ * (the EP curve behind return-period loss reports).  1 <= m <= 256.
+ * Results to HOST out; synchronises `stream`. */
+ARA_API ara_status ara_ep(const double* ylt, uint64_t n, const double* thresholds, uint32_t m, double* out,
+                          void* stream);
+
+/* Program / portfolio totals (a portfolio groups programs, a program groups layers):
+ * out[g * n + t] = sum over layers l with group[l] == g, in layer order, of ylt[l * n + t].
+ * ylt, out: DEVICE ([num_layers][n], [num_groups][n]); group: HOST, num_layers entries < num_groups;
+ * num_layers <= 128.  Asynchronous. */
+ARA_API ara_status ara_sum_layers(const double* ylt, uint32_t num_layers, uint64_t n, const uint32_t* group,
+                                  uint32_t num_groups, double* out, void* stream);
 
 /* Host-only memory accounting of one layer's direct-access table: bytes of the
  * (C+1)-row table and its row stride.  No device needed. */

@@ -158,6 +158,15 @@ def ep(y: np.ndarray, thresholds: Sequence[float]) -> np.ndarray:
     return out[:x.size]
 
 
+def layer_totals(ylt: np.ndarray, group: Sequence[int], num_groups: int) -> np.ndarray:
+    """Program / portfolio totals: out[g][t] = sum of ylt[l][t] over layers l of group g, in layer
+    order.  Plain loop."""
+    out = np.zeros((num_groups, ylt.shape[1]))
+    for l, g in enumerate(group):
+        out[g] = out[g] + ylt[l]
+    return out
+
+
 def trial_detail(catalog_size: int, ids: Sequence[int], elts, layer, lookup: int = LOOKUP_BINARY):
     """(o, S, a, ylt) for one trial under one layer."""
     ids = np.ascontiguousarray(ids, dtype=np.uint32)

@@ -19,7 +19,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-I", INCLUDE, "-Xptxas", "-warn-spills"]
 
 LIBS = {
-    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_api.cu", "metrics.cu", "kernels_presence.cu", "kernels_dense.cu", "kernels_study.cu")],
+    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_api.cu", "metrics.cu", "kernels_presence.cu", "kernels_presence_mid.cu", "kernels_presence_wide.cu", "kernels_dense.cu", "kernels_study.cu", "outputs.cu")],
     "libara_synth.so": [os.path.join(HERE, "synth", "synth.cu")],
 }
 DEPS = {

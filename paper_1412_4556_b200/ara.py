@@ -28,7 +28,8 @@ STUDY_INTERLEAVED, STUDY_INDEPENDENT, STUDY_SORTED = 0, 1, 2
 ARA_MAX_ELTS_PER_LAYER = 128
 
 #: every symbol include/ara.h declares (checked by tests/test_abi.py against the header and the .so)
-EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_host", "ara_run_study", "ara_check", "ara_pml_tvar", "ara_pml",
+EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_ex", "ara_run_host", "ara_run_study", "ara_aal", "ara_ep",
+           "ara_sum_layers", "ara_check", "ara_pml_tvar", "ara_pml",
            "ara_tvar", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
            "ara_layer_info", "ara_layer_stats", "ara_table_row", "ara_status_string", "ara_last_error", "ara_version")
 
@@ -75,6 +76,10 @@ def lib() -> ctypes.CDLL:
             "ara_destroy": (None, [vp]),
             "ara_run": (st, [vp, ctypes.POINTER(_Yet), dp, vp]),
             "ara_run_host": (st, [vp, ctypes.POINTER(_Yet), dp, vp]),
+            "ara_run_ex": (st, [vp, ctypes.POINTER(_Yet), dp, dp, vp]),
+            "ara_aal": (st, [dp, u64, dp, vp]),
+            "ara_ep": (st, [dp, u64, dp, u32, dp, vp]),
+            "ara_sum_layers": (st, [dp, u32, u64, dp, u32, dp, vp]),
             "ara_run_study": (st, [vp, ctypes.c_int, ctypes.POINTER(_Yet), dp, vp]),
             "ara_check": (st, [vp, vp]),
             "ara_pml_tvar": (st, [dp, u64, dp, u32, dp, dp, vp]),
@@ -222,6 +227,14 @@ class Context:
         y = _yet_struct(event_ids, offsets, n, events_per_trial)
         _check(lib().ara_run(self._h, ctypes.byref(y), _dptr(ylt), _stream_ptr(stream)), "ara_run")
 
+    def ara_run_ex(self, event_ids, ylt, olt=None, offsets=None, events_per_trial: int = 0,
+                   num_trials: Optional[int] = None, stream=None) -> None:
+        """ara_run plus the occurrence-basis table (largest occurrence-net loss per trial)."""
+        n = num_trials if num_trials is not None else (offsets.numel() - 1 if offsets is not None else
+                                                       event_ids.numel() // max(1, events_per_trial))
+        y = _yet_struct(event_ids, offsets, n, events_per_trial)
+        _check(lib().ara_run_ex(self._h, ctypes.byref(y), _dptr(ylt), _dptr(olt), _stream_ptr(stream)), "ara_run_ex")
+
     def ara_run_host(self, event_ids, ylt_host, offsets=None, events_per_trial: int = 0,
                      num_trials: Optional[int] = None, stream=None) -> None:
         """Host YET (pinned for overlap) -> host YLT.  Synchronous, includes the validity check."""
@@ -304,6 +317,27 @@ def ara_tvar(ylt, rps: Sequence[float], stream=None) -> np.ndarray:
     out = np.zeros(max(1, r.size))
     _check(lib().ara_tvar(_dptr(ylt), _numel(ylt), _dptr(r), r.size, _dptr(out), _stream_ptr(stream)), "ara_tvar")
     return out[:r.size]
+
+
+def ara_aal(ylt, stream=None, n: Optional[int] = None) -> float:
+    out = ctypes.c_double()
+    _check(lib().ara_aal(_dptr(ylt), _numel(ylt) if n is None else n, ctypes.addressof(out), _stream_ptr(stream)),
+           "ara_aal")
+    return out.value
+
+
+def ara_ep(ylt, thresholds: Sequence[float], stream=None) -> np.ndarray:
+    x = np.ascontiguousarray(thresholds, dtype=np.float64)
+    out = np.zeros(max(1, x.size))
+    _check(lib().ara_ep(_dptr(ylt), _numel(ylt), _dptr(x), x.size, _dptr(out), _stream_ptr(stream)), "ara_ep")
+    return out[:x.size]
+
+
+def ara_sum_layers(ylt, group: Sequence[int], num_groups: int, out, stream=None) -> None:
+    """ylt: CUDA [layers, n]; out: CUDA [num_groups, n]."""
+    g = np.ascontiguousarray(group, dtype=np.uint32)
+    _check(lib().ara_sum_layers(_dptr(ylt), g.size, ylt.shape[1], _dptr(g), num_groups, _dptr(out),
+                                _stream_ptr(stream)), "ara_sum_layers")
 
 
 def ara_unshard(gathered, num_shards: int, shard_cap: int, num_layers: int, starts: Sequence[int], ylt,

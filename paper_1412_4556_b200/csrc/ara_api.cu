@@ -49,10 +49,13 @@ static uint32_t row_floats(uint32_t J) {
 // ------------------------------------------------------------------------------------------ variants
 static void variants_for(int kind, uint32_t jpad, std::vector<const Variant*>& out) {
   out.clear();
-  int n = 0;
-  const Variant* t = kind == KIND_PRESENCE ? presence_variants(&n) : dense_variants(&n);
-  for (int i = 0; i < n; ++i)
-    if (t[i].jpad == jpad) out.push_back(&t[i]);
+  const Variant* (*tables[3])(int*) = {presence_variants_narrow, presence_variants_mid, presence_variants_wide};
+  for (int k = 0; k < (kind == KIND_DENSE ? 1 : 3); ++k) {
+    int n = 0;
+    const Variant* t = kind == KIND_DENSE ? dense_variants(&n) : tables[k](&n);
+    for (int i = 0; i < n; ++i)
+      if (t[i].jpad == jpad) out.push_back(&t[i]);
+  }
 }
 
 // ------------------------------------------------------------------------------------------ context
@@ -235,7 +238,7 @@ static const Variant* pick(const ara_ctx* c, const Layer& L) {
 }
 
 static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, const uint64_t* offsets,
-                               uint64_t num_trials, uint64_t num_events, uint32_t K, double* ylt,
+                               uint64_t num_trials, uint64_t num_events, uint32_t K, double* ylt, double* olt,
                                cudaStream_t stream) {
   if (num_trials == 0) return ARA_OK;
   const Variant* var = pick(c, L);
@@ -251,6 +254,7 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
   p.jpad = L.jpad;
   p.l2_hints = c->l2_policy == 1 ? 0u : 1u;
   p.ylt = ylt;
+  p.olt = olt;
   p.err = c->d_err;
   p.r2 = L.r2;
   p.l2 = L.l2;
@@ -276,6 +280,7 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
     p.fold_magic = UINT64_MAX / p.fold_words + 1;
     dyn_smem = ((size_t)p.fold_words + (size_t)var->NW * kQueue) * 4;
     ARA_CUDA(cudaFuncSetAttribute((const void*)var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
+    ARA_CUDA(cudaFuncSetAttribute((const void*)var->fn_olt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
   }
   int bps = c->blocks_per_sm;
   if (bps <= 0) {
@@ -305,14 +310,15 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  ARA_CUDA(cudaLaunchKernelEx(&cfg, var->fn, p));
+  ARA_CUDA(cudaLaunchKernelEx(&cfg, olt ? var->fn_olt : var->fn, p));
   return ARA_OK;
 }
 
 static ara_status run_layers(ara_ctx* c, const uint32_t* ids, const uint64_t* offsets, uint64_t num_trials,
-                             uint64_t num_events, uint32_t K, double* ylt, uint64_t ld, cudaStream_t s) {
+                             uint64_t num_events, uint32_t K, double* ylt, double* olt, uint64_t ld, cudaStream_t s) {
   for (size_t l = 0; l < c->layers.size(); ++l) {
-    ara_status st = launch_layer(c, c->layers[l], ids, offsets, num_trials, num_events, K, ylt + l * ld, s);
+    ara_status st = launch_layer(c, c->layers[l], ids, offsets, num_trials, num_events, K, ylt + l * ld,
+                                 olt ? olt + l * ld : nullptr, s);
     if (st) return st;
   }
   return ARA_OK;
@@ -504,7 +510,7 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
 
 void ara_destroy(ara_ctx* ctx) { destroy_ctx(ctx); }
 
-ara_status ara_run(ara_ctx* c, const ara_yet* yet, double* ylt, void* stream) {
+ara_status ara_run_ex(ara_ctx* c, const ara_yet* yet, double* ylt, double* olt, void* stream) {
   if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
   ara_status st = check_yet(yet);
   if (st) return st;
@@ -512,7 +518,11 @@ ara_status ara_run(ara_ctx* c, const ara_yet* yet, double* ylt, void* stream) {
   if (!ylt) return set_error(ARA_E_ARG, "ylt is NULL");
   DeviceGuard guard(c->device);
   return run_layers(c, yet->event_ids, yet->trial_offsets, yet->num_trials, yet->num_events,
-                    yet->events_per_trial, ylt, yet->num_trials, (cudaStream_t)stream);
+                    yet->events_per_trial, ylt, olt, yet->num_trials, (cudaStream_t)stream);
+}
+
+ara_status ara_run(ara_ctx* c, const ara_yet* yet, double* ylt, void* stream) {
+  return ara_run_ex(c, yet, ylt, nullptr, stream);
 }
 
 ara_status ara_check(ara_ctx* c, void* stream) {
@@ -604,7 +614,8 @@ ara_status ara_run_host(ara_ctx* c, const ara_yet* yet, double* ylt_host, void* 
     }
     ARA_CUDA(cudaEventRecord(c->ev_copied[i], c->copy_stream));
     ARA_CUDA(cudaStreamWaitEvent(s, c->ev_copied[i], 0));
-    st = run_layers(c, c->st_ids[i], hoff ? c->st_off[i] : nullptr, t1 - t0, q1 - q0, K, c->st_ylt[i], t1 - t0, s);
+    st = run_layers(c, c->st_ids[i], hoff ? c->st_off[i] : nullptr, t1 - t0, q1 - q0, K, c->st_ylt[i], nullptr,
+                    t1 - t0, s);
     if (st) return st;
     for (uint64_t l = 0; l < L; ++l)
       ARA_CUDA(cudaMemcpyAsync(ylt_host + l * N + t0, c->st_ylt[i] + l * (t1 - t0), (t1 - t0) * 8,

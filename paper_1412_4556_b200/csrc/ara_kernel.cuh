@@ -39,6 +39,7 @@ struct LayerParams {
   uint32_t jpad;             // row stride in floats
   uint32_t l2_hints;         // 1: evict_last / evict_first policies; 0: evict_normal
   double* ylt;               // this layer's YLT row (num_trials doubles)
+  double* olt;               // this layer's OLT row (largest occurrence-net loss per trial) or nullptr
   unsigned* err;             // bit0: id out of range, bit1: bad offsets
   double r2, l2, r3, l3;     // FT2, FT3
   const uint32_t* present;   // presence bitmap: bit e set iff row e holds a non-zero loss (presence kernel)
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(256) ara_layer_kernel(const __grid_constant__ 
       e = b + p.K;
     }
     double S = 0.0;  // leader's running sum of occurrence-net losses (step 4)
+    double M = 0.0;  // leader's largest occurrence-net loss (OLT)
     for (uint64_t k0 = b; k0 < e; k0 += (uint64_t)RG * U) {
       uint32_t id[U];
 #pragma unroll
@@ -251,11 +253,20 @@ __global__ void __launch_bounds__(256) ara_layer_kernel(const __grid_constant__ 
           }
         }
         // Step 3: occurrence terms FT2; step 4: accumulate (leader lane of the row group).
-        if (s != 0.0 && g == 0) S += clamp_terms(s, R2, L2);
+        if (s != 0.0 && g == 0) {
+          const double o = clamp_terms(s, R2, L2);
+          S += o;
+          M = o > M ? o : M;
+        }
       }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(FULL, S, off);
+    if (p.olt) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(FULL, M, off));
+      if (lane == 0) p.olt[t] = M;
+    }
     bad = __reduce_or_sync(FULL, bad);
     if (lane == 0) {
       p.ylt[t] = clamp_terms(S, p.r3, p.l3);  // step 4: aggregate terms FT3 on S_n

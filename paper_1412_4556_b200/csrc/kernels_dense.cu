@@ -6,7 +6,7 @@ namespace ara {
 
 #define ARA_DENSE(V_, NV_, G_, U_) \
   {KIND_DENSE, (uint32_t)((V_) * (NV_)), V_, NV_, G_, U_, 0, ara_layer_kernel<V_, NV_, G_, U_>, \
-   "ara_layer_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",U=" #U_ ">"}
+   "ara_layer_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",U=" #U_ ">", ara_layer_kernel<V_, NV_, G_, U_>}
 
 static const Variant kTable[] = {
     // ---- dense kernels: every occurrence gathers its row (the plain direct-access path)

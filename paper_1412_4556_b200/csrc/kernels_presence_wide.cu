@@ -1,0 +1,28 @@
+// kernels_presence_wide.cu -- instantiations of the presence-bitmap ARA kernel.
+#include "presence_kernel.cuh"
+#include "variants.cuh"
+
+namespace ara {
+
+#define ARA_PRES(V_, NV_, G_, NW_) \
+  {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, G_, 0, NW_, ara_presence_kernel<V_, NV_, G_, NW_, false>, \
+   "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",NW=" #NW_ ">", ara_presence_kernel<V_, NV_, G_, NW_, true>}
+
+
+static const Variant kTable[] = {
+    // first per row width = default (B200 sweeps)
+    ARA_PRES(8, 10, 16, 16), ARA_PRES(8, 10, 8, 16), ARA_PRES(8, 10, 16, 24),
+    ARA_PRES(8, 11, 16, 16), ARA_PRES(8, 11, 8, 16), ARA_PRES(8, 11, 16, 24),
+    ARA_PRES(8, 12, 16, 16), ARA_PRES(8, 12, 8, 16), ARA_PRES(8, 12, 16, 24),
+    ARA_PRES(8, 13, 16, 16), ARA_PRES(8, 13, 8, 16), ARA_PRES(8, 13, 16, 24),
+    ARA_PRES(8, 14, 16, 16), ARA_PRES(8, 14, 8, 16), ARA_PRES(8, 14, 16, 24),
+    ARA_PRES(8, 15, 16, 16), ARA_PRES(8, 15, 8, 16), ARA_PRES(8, 15, 16, 24),
+    ARA_PRES(8, 16, 16, 16), ARA_PRES(8, 16, 8, 16), ARA_PRES(8, 16, 16, 24),
+};
+
+const Variant* presence_variants_wide(int* n) {
+  *n = (int)(sizeof(kTable) / sizeof(kTable[0]));
+  return kTable;
+}
+
+}  // namespace ara

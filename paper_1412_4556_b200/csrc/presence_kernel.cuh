@@ -61,7 +61,7 @@ struct RowBatch {
   }
 
   __device__ __forceinline__ void consume_round(int r, const LayerParams& p, int lane, const double* s_r1,
-                                                const double* s_l1, double& S) const {
+                                                const double* s_l1, double& S, double& M) const {
     const int g = lane % G;
     const float(&xr)[NVL][V] = x[kAsync ? r : 0];
     // Steps 1-2: FT1 on each of the row's losses, summed across the layer's ELTs.  Branch-free: an
@@ -78,7 +78,11 @@ struct RowBatch {
 #pragma unroll
       for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
     }
-    if (g == 0) S += clamp_fast(sum, p.r2, p.l2);  // step 3 (FT2); step 4 accumulation (exact +0 if sum 0)
+    if (g == 0) {  // step 3 (FT2); step 4 accumulation (exact +0 if sum 0)
+      const double o = clamp_fast(sum, p.r2, p.l2);
+      S += o;
+      M = o > M ? o : M;
+    }
   }
 
   // G == 1 only: occurrence-net loss o = FT2(sum_j FT1(x_j)) of the lane's own row (slot = lane).
@@ -97,12 +101,12 @@ struct RowBatch {
   // Async: issue all rounds now, consume later.  Sync: issue+consume round by round.
   __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, unsigned head, int n,
                                         int lane, uint64_t pol_tab, const double* s_r1, const double* s_l1,
-                                        double& S) {
+                                        double& S, double& M) {
 #pragma unroll
     for (int r = 0; r < G; ++r) {
       if (r * RG >= n) break;  // warp-uniform
       issue_round(r, p, q, head, n, lane, pol_tab);
-      if constexpr (!kAsync) consume_round(r, p, lane, s_r1, s_l1, S);
+      if constexpr (!kAsync) consume_round(r, p, lane, s_r1, s_l1, S, M);
     }
     if constexpr (kAsync) {
       for (int r = (n + RG - 1) / RG; r < G; ++r)  // rounds past n hold nothing
@@ -114,10 +118,10 @@ struct RowBatch {
   }
 
   __device__ __forceinline__ void consume(const LayerParams& p, int lane, const double* s_r1, const double* s_l1,
-                                          double& S) const {
+                                          double& S, double& M) const {
     if constexpr (kAsync) {
 #pragma unroll
-      for (int r = 0; r < G; ++r) consume_round(r, p, lane, s_r1, s_l1, S);
+      for (int r = 0; r < G; ++r) consume_round(r, p, lane, s_r1, s_l1, S, M);
     }
   }
 };
@@ -193,7 +197,9 @@ struct WarpTrials {
 // trial is always accumulated by lane i mod 32 (a shuffle rotates each batch into that frame), and the
 // lanes are combined by the same xor-tree -- so a trial's fp64 summation order depends only on its own
 // ids, never on its neighbours, the sharding or the launch shape.
-template <int V, int NV, int G, int NW>
+// OLT: also track the largest occurrence-net loss per trial (ara_run_ex); a separate instantiation so
+// the plain YLT path carries no extra registers.
+template <int V, int NV, int G, int NW, bool OLT>
 __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_constant__ LayerParams p) {
   constexpr int JP = V * NV;
   constexpr unsigned FULL = 0xffffffffu;
@@ -243,6 +249,8 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   const bool carry = kCarry && (C < 0x80000000u);      // the parity tag lives in bit 31 of a queue word
 
   double S0 = 0.0, S1 = 0.0;  // per-lane partial sums of the (<= 2) open trials, by parity
+  double M0 = 0.0, M1 = 0.0;  // per-lane largest occurrence-net loss of those trials (OLT)
+  constexpr bool want_olt = OLT;
   unsigned head = 0, count = 0;  // ring of queued, not yet issued hits
   uint32_t issued = 0;           // stream position of the next hit to issue
   Batch rows;
@@ -255,7 +263,19 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(FULL, S, off);
     if (lane == 0) p.ylt[wt.trial[a]] = clamp_terms(S, p.r3, p.l3);  // step 4: aggregate terms FT3
-    if (kCarry && a) S1 = 0.0; else S0 = 0.0;
+    if constexpr (OLT) {  // the trial's largest occurrence-net loss (order-free, exact)
+      double M = (kCarry && a) ? M1 : M0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(FULL, M, off));
+      if (lane == 0) p.olt[wt.trial[a]] = M;
+    }
+    if (kCarry && a) {
+      S1 = 0.0;
+      M1 = 0.0;
+    } else {
+      S0 = 0.0;
+      M0 = 0.0;
+    }
     __syncwarp();
     if (lane == 0) wt.state[a] = 0u;
     __syncwarp();
@@ -272,6 +292,10 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       if constexpr (kCarry) {
         const double o = rows.row_loss(p, s_r1, s_l1, pol_tab);
         const bool mine = lane < bn;
+        if (want_olt && mine) {  // the maximum needs no canonical order: the source lane keeps it
+          if (btag) M1 = o > M1 ? o : M1;
+          else M0 = o > M0 ? o : M0;
+        }
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
           if (wt.state[a] == 0u) continue;  // warp-uniform
@@ -283,7 +307,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
           }
         }
       } else {
-        if constexpr (!kCarry) rows.consume(p, lane, s_r1, s_l1, S0);
+        if constexpr (!kCarry) rows.consume(p, lane, s_r1, s_l1, S0, M0);
       }
       bn = 0;
     }
@@ -298,7 +322,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     if constexpr (kCarry) {
       rows.issue(p, q, head, n, lane, pol_tab);
     } else {
-      rows.issue(p, q, head, n, lane, pol_tab, s_r1, s_l1, S0);
+      rows.issue(p, q, head, n, lane, pol_tab, s_r1, s_l1, S0, M0);
     }
     __syncwarp();
     bstart = issued;

@@ -17,10 +17,13 @@ struct Variant {
   int V, NV, G, U, NW;  // U: dense rows per group; NW: presence warps per block (fixed block size)
   KernelFn fn;
   const char* name;
+  KernelFn fn_olt;  // the same kernel also producing the occurrence loss table (presence kernels; dense: fn)
 };
 
 // Defined in kernels_presence.cu / kernels_dense.cu.  First entry per row width is the default.
-const Variant* presence_variants(int* n);
+const Variant* presence_variants_narrow(int* n);  // rows of <= 16 columns
+const Variant* presence_variants_mid(int* n);     // 17..72 columns
+const Variant* presence_variants_wide(int* n);    // 73..128 columns
 const Variant* dense_variants(int* n);
 
 }  // namespace ara

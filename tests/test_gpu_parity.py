@@ -409,3 +409,63 @@ def test_section_4b_study_layouts(cuda_device, layout):
                       offsets=torch.from_numpy(y.offsets.view(np.int64)).cuda())
     torch.cuda.synchronize()
     assert np.all(within_tol(out.cpu().numpy(), want))
+
+
+# ------------------------------------------------------------------ N4 outputs
+@pytest.mark.parametrize("name", ["T", "V"])
+def test_olt_matches_oracle_every_kernel(cuda_device, name):
+    cfg = synth.Config.load(name)
+    elts = synth.make_elts(cfg)
+    yet = synth.make_yet(cfg)
+    wy, wo = oracle.ylt_olt(cfg.catalog_size, yet.event_ids, yet.offsets, yet.num_trials, yet.events_per_trial,
+                            oracle.config_elts(cfg, elts), oracle.config_layers(cfg))
+    ctx = ara.context_for_config(cfg, elts)
+    ids = torch.from_numpy(yet.event_ids.view(np.int32)).cuda()
+    off = None if yet.offsets is None else torch.from_numpy(yet.offsets.view(np.int64)).cuda()
+    for k, v in variants(ctx):
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
+        ctx.ara_set_option(ara.ARA_OPT_VARIANT, v)
+        y = torch.zeros((1, yet.num_trials), dtype=torch.float64, device=cuda_device)
+        o = torch.full((1, yet.num_trials), -1.0, dtype=torch.float64, device=cuda_device)
+        ctx.ara_run_ex(ids, y, o, offsets=off, events_per_trial=yet.events_per_trial, num_trials=yet.num_trials)
+        ctx.ara_check()
+        assert np.array_equal(o.cpu().numpy(), wo), (k, v)          # a maximum of identical values: exact
+        assert np.all(within_tol(y.cpu().numpy(), wy))
+    ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_AUTO)
+
+
+def test_olt_wide_rows_and_empty_trials(cuda_device):
+    C, elts, layer, _, _, _ = _small_problem(100, seed=9)
+    rng = np.random.default_rng(3)
+    trials = [list(rng.integers(1, C + 1, size=k)) for k in (0, 1, 5, 40, 0, 100)]
+    ids, off = ragged(trials)
+    wy, wo = oracle.ylt_olt(C, ids, off, len(trials), 0, elts, [layer])
+    ctx = _ctx_from(C, elts, [layer])
+    for k, v in variants(ctx):
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
+        ctx.ara_set_option(ara.ARA_OPT_VARIANT, v)
+        y = torch.zeros((1, len(trials)), dtype=torch.float64, device=cuda_device)
+        o = torch.full((1, len(trials)), -1.0, dtype=torch.float64, device=cuda_device)
+        ctx.ara_run_ex(torch.from_numpy(ids.view(np.int32)).cuda(), y, o,
+                       offsets=torch.from_numpy(off.view(np.int64)).cuda())
+        assert np.array_equal(o.cpu().numpy(), wo) and np.array_equal(y.cpu().numpy(), wy), (k, v)
+
+
+def test_aal_ep_and_layer_totals(cuda_device):
+    rng = np.random.default_rng(8)
+    for n in (1, 1000, 1_000_003):
+        y = np.floor(rng.exponential(1e6, n)) * (rng.random(n) > 0.3)
+        d = torch.from_numpy(y).cuda()
+        assert ara.ara_aal(d) == oracle.aal(y) or abs(ara.ara_aal(d) / oracle.aal(y) - 1) < 1e-12
+        xs = [0.0, 1.0, 5e5, 1e6, 3e6, float(y.max()), float(y.max()) + 1]
+        assert np.array_equal(ara.ara_ep(d, xs), oracle.ep(y, xs))
+    ints = np.floor(rng.exponential(1e6, 100_000))
+    assert ara.ara_aal(torch.from_numpy(ints).cuda()) == oracle.aal(ints)  # integer-valued: exact
+    cfg = synth.Config.load("T")
+    L, n = 5, 777
+    ylt = rng.random((L, n)) * 1e6
+    group = [0, 1, 0, 2, 1]
+    out = torch.zeros((3, n), dtype=torch.float64, device=cuda_device)
+    ara.ara_sum_layers(torch.from_numpy(ylt).cuda(), group, 3, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.layer_totals(ylt, group, 3))
