@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--sweep", action="store_true", help="launch-shape sweep (E8); extra JSON lines to stderr")
     ap.add_argument("--cpu-sample", type=int, default=65536, help="trials in the cpu_baseline sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cold/cpu legs")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: exercise the multi-rank flow with several ranks sharing one GPU (testing only)")
     ap.add_argument("--study", action="store_true",
                     help="Section IV.B data-structure study (interleaved / independent / sorted ELTs); JSON lines to stderr")
     return ap.parse_args()
@@ -178,8 +180,12 @@ def main():
 
     world, rank, local = dist_env()
     if world > 1:
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())

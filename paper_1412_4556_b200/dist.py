@@ -64,7 +64,12 @@ def gather_ylt(local_ylt, num_trials: int, group=None):
         send = torch.empty((L, cap), dtype=local_ylt.dtype, device=local_ylt.device)
         send[:, :local_ylt.shape[1]].copy_(local_ylt)  # plumbing: pad the send buffer (D2D copy)
     recv = torch.empty((world, L, cap), dtype=local_ylt.dtype, device=local_ylt.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(recv.view(-1), send.reshape(-1), group=group)
+    else:  # gloo (testing several ranks on one GPU): the same gather through host memory
+        host = torch.empty(world * L * cap, dtype=local_ylt.dtype)
+        dist.all_gather_into_tensor(host, send.reshape(-1).cpu(), group=group)
+        recv.view(-1).copy_(host)
     full = torch.empty((L, num_trials), dtype=local_ylt.dtype, device=local_ylt.device)
     ara.ara_unshard(recv, world, cap, L, starts, full)
     return full
