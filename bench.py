@@ -498,13 +498,12 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
     for v in range(nv):
         for bt in (128, 256):
             for bps in (0,) if info[0]["variant"].startswith("ara_presence") else (0, 2, 3, 4, 6, 8):
-                for pol in (0, 1, 2, 10, 12, 14):
+                for pol in (0, 1, 2):
                     try:
                         ctx.ara_set_option(ara.ARA_OPT_VARIANT, v)
                         ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, bt)
                         ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, bps)
-                        ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, pol if pol < 10 else 0)
-                        ctx.ara_set_option(ara.ARA_OPT_PREFETCH, pol - 8 if pol >= 10 else 0)
+                        ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, pol)
                     except ara.AraError:
                         continue
                     for _ in range(2):
@@ -522,7 +521,6 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
     ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, 0)
     ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, 0)
     ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, 0)
-    ctx.ara_set_option(ara.ARA_OPT_PREFETCH, 0)
 
 
 if __name__ == "__main__":

@@ -203,16 +203,13 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           1 dense: every occurrence gathers its full row.  Identical results (an
  *                           all-zero row contributes exactly 0, reading c9).
  *                           Selecting a kernel resets ARA_OPT_VARIANT to 0.
- *   ARA_OPT_PREFETCH        presence kernel: also prefetch the YET window this many windows ahead
- *                           into L2 (0 = off, the default)
  * ARA_OPT_BLOCK_THREADS applies to the dense kernel; the presence kernel fixes its block size. */
 typedef enum {
   ARA_OPT_BLOCK_THREADS = 1,
   ARA_OPT_BLOCKS_PER_SM = 2,
   ARA_OPT_L2_POLICY = 3,
   ARA_OPT_VARIANT = 4,
-  ARA_OPT_KERNEL = 5,
-  ARA_OPT_PREFETCH = 6
+  ARA_OPT_KERNEL = 5
 } ara_option;
 ARA_API ara_status ara_set_option(ara_ctx* ctx, ara_option opt, int64_t value);
 ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);

@@ -96,7 +96,6 @@ struct ara_ctx {
   int kernel = -1;  // KernelKind, or -1 = per-layer automatic choice
   int persist_max = 0, window_max = 0;
   int smem_optin = 0;
-  int pf_dist = 0;  // presence kernel L2 prefetch distance (windows)
   // end-to-end host path
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
@@ -274,7 +273,6 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
     if (budget < 4096) return set_error(ARA_E_UNSUPPORTED, "no shared memory left for the presence bitmap");
     p.present = L.present;
     p.rec = L.rec;
-    p.pf_dist = (uint32_t)c->pf_dist;
     p.present_words = L.present_words;
     p.fold_words = (uint32_t)std::min<int64_t>(L.present_words, budget / 4);
     p.fold_magic = UINT64_MAX / p.fold_words + 1;
@@ -750,10 +748,6 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
           return set_error(ARA_E_ARG, "variant %lld not available", (long long)v);
       c->variant = (int)v;
       return ARA_OK;
-    case ARA_OPT_PREFETCH:
-      if (v < 0 || v > 64) return set_error(ARA_E_ARG, "prefetch distance in [0, 64] windows");
-      c->pf_dist = (int)v;
-      return ARA_OK;
     case ARA_OPT_KERNEL:
       if (v < -1 || v > 1) return set_error(ARA_E_ARG, "kernel in {-1 auto, 0 presence, 1 dense}");
       c->kernel = (int)v;
@@ -771,7 +765,6 @@ ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
     case ARA_OPT_L2_POLICY: *v = c->l2_policy; return ARA_OK;
     case ARA_OPT_VARIANT: *v = c->variant; return ARA_OK;
     case ARA_OPT_KERNEL: *v = c->kernel; return ARA_OK;
-    case ARA_OPT_PREFETCH: *v = c->pf_dist; return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }

@@ -47,7 +47,6 @@ struct LayerParams {
   uint32_t fold_words;       // bitmap words held in shared memory (<= present_words; folded mod fold_words)
   uint64_t fold_magic;       // floor((2^64 - 1) / fold_words) + 1: fast word % fold_words (Lemire)
   const uint4* rec;          // per-event sparse row record (presence kernel, rows <= 16 columns)
-  uint32_t pf_dist;          // presence kernel: L2 prefetch distance in windows (0 = off)
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
 
@@ -137,8 +136,6 @@ __device__ __forceinline__ void st_shared_if(uint32_t* ptr, uint32_t v, bool pre
                :: "r"((uint32_t)__cvta_generic_to_shared(ptr)), "r"(v), "r"((int)pred) : "memory");
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" :: "l"(ptr)); }
-
 // Warp-synchronous primitives as inline PTX for full-warp, converged call sites (the presence kernel's
 // scan): avoids the divergence-handling slow paths nvcc wraps around the intrinsics.
 __device__ __forceinline__ unsigned ballot_full(bool p) {
@@ -152,6 +149,22 @@ __device__ __forceinline__ bool any_full(bool p) {
   asm volatile("{\n .reg .pred q, o;\n setp.ne.u32 q, %1, 0;\n vote.sync.any.pred o, q, 0xffffffff;\n selp.u32 %0, 1, 0, o;\n}"
                : "=r"(r) : "r"((unsigned)p));
   return r != 0;
+}
+
+// 32-bit shared-window helpers (the shared-memory base is computed once per kernel).
+__device__ __forceinline__ void sts_u32_if(uint32_t saddr, uint32_t v, bool pred) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.shared.u32 [%0], %1;\n}"
+               :: "r"(saddr), "r"(v), "r"((int)pred) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
 }
 
 // V: floats per vector load; NV: vectors per row (jpad = V*NV); G: lanes per row (power of 2 <= 32);

@@ -216,6 +216,8 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   const int lane = threadIdx.x & 31;
   uint32_t* q = smem + p.fold_words + warp * kQueue;
   WarpTrials& wt = s_wt[warp];
+  const uint32_t bits_s = (uint32_t)__cvta_generic_to_shared(bits);  // 32-bit shared addresses
+  const uint32_t q_s = (uint32_t)__cvta_generic_to_shared(q);
 
   for (int j = threadIdx.x; j < JPS; j += blockDim.x) {
     s_r1[j] = j < JP ? p.r1[j] : 0.0;
@@ -386,12 +388,11 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     };
     // Full windows (16-B aligned trial, 128 ids inside the trial) stream through a running per-lane
     // pointer with no bounds checks; the trial's last partial window (or an unaligned trial) goes
-    // through the checked loader.  One window is held ahead in registers; optionally lanes 0-3 also
-    // prefetch the window pf_dist ahead into L2.
+    // through the checked loader.  One window is held ahead in registers (an extra L2 prefetch of
+    // windows further ahead measured slower).
     const uint32_t nwin = (len + 127) / 128;
     const uint32_t nfull = vec ? len / 128 : 0u;
     const uint4* lp = reinterpret_cast<const uint4*>(base) + lane;
-    const uint32_t pfd = p.pf_dist;
     auto load_win = [&](uint32_t w) -> uint4 {
       if (w < nfull) return ld_ids4(reinterpret_cast<const uint32_t*>(lp + (size_t)w * 32), pol_yet);
       if (w < nwin) return load4(w * 128);
@@ -401,10 +402,6 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     uint4 cur = load_win(0);
     for (uint32_t w = 0; w < nwin; ++w) {
       const uint4 nxt = load_win(w + 1);
-      if (pfd && lane < 4) {
-        const uint32_t at = (w + pfd) * 128 + 32u * lane;
-        if (at < len) prefetch_l2(base + at);
-      }
       const uint32_t id[4] = {cur.x, cur.y, cur.z, cur.w};
       if (w < nfull) {  // validity is checked once per trial from the running extremes
         mxv = max(mxv, max(max(id[0], id[1]), max(id[2], id[3])));
@@ -419,7 +416,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       for (int u = 0; u < 4; ++u) {
         uint32_t wd = min(id[u], C) >> 5;  // an invalid id > C is clamped into the bitmap
         wd = fold_small ? min(wd, wd - fw) : (uint32_t)__umul64hi(fmagic * (uint64_t)wd, (uint64_t)fw);
-        hit[u] = (bits[wd] >> (id[u] & 31u)) & 1u;  // id 0 -> bit 0 of word 0, never set
+        hit[u] = (lds_u32(bits_s + 4u * wd) >> (id[u] & 31u)) & 1u;  // id 0 -> bit 0 of word 0, never set
       }
       // Append the hits in a fixed order that depends only on the window: per pair of slots, first the
       // lanes' first hit of the pair (lanes ascending), then -- only if some lane hit both -- the
@@ -430,12 +427,12 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
         const bool any = ha || hb;
         const uint32_t first = tag | (ha ? id[2 * h] : id[2 * h + 1]);
         const unsigned m = __ballot_sync(FULL, any);
-        st_shared_if(q + ((head + count + __popc(m & lt)) & (kQueue - 1)), first, any);
+        sts_u32_if(q_s + 4u * ((head + count + __popc(m & lanemask_lt())) & (kQueue - 1)), first, any);
         count += __popc(m);
         const bool both = ha && hb;
         if (__any_sync(FULL, both)) {  // rare: ~1% of lanes per pair
           const unsigned m2 = __ballot_sync(FULL, both);
-          st_shared_if(q + ((head + count + __popc(m2 & lt)) & (kQueue - 1)), tag | id[2 * h + 1], both);
+          sts_u32_if(q_s + 4u * ((head + count + __popc(m2 & lanemask_lt())) & (kQueue - 1)), tag | id[2 * h + 1], both);
           count += __popc(m2);
         }
         while (count >= 32) issue(32);  // warp-uniform; at most 31 + 64 = 95 < kQueue queued
