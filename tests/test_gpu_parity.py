@@ -466,3 +466,52 @@ def test_aal_ep_and_layer_totals(cuda_device):
     ara.ara_sum_layers(torch.from_numpy(ylt).cuda(), group, 3, out)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), oracle.layer_totals(ylt, group, 3))
+
+
+# ------------------------------------------------------------------ more edge cases
+def test_degenerate_shapes(cuda_device):
+    # catalogue of one event; one trial; one ELT; trials made only of that event
+    elts = [(np.array([1], np.uint32), np.array([123.0], np.float32), (0.0, INF))]
+    layer = ([0], (0.0, INF), (0.0, INF))
+    for N, K in ((1, 1), (1, 5), (37, 3)):
+        yet = np.ones(N * K, np.uint32)
+        want = oracle.ylt(1, yet, None, N, K, elts, [layer])
+        ctx = _ctx_from(1, elts, [layer])
+        for k, v in variants(ctx):
+            assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=k, variant=v), want)
+    # K = 0: every trial empty
+    ctx = _ctx_from(1, elts, [layer])
+    y = gpu_ylt(None, ctx, np.zeros(0, np.uint32), K=0, num_trials=4)
+    assert np.array_equal(y, np.zeros((1, 4)))
+
+
+def test_multi_layer_mixed_widths_with_olt_every_kernel(cuda_device):
+    C, elts, layer, yet, N, K = _small_problem(40, seed=13)
+    layers = [layer, ([3, 1, 7, 9], (10.0, 1e6), (0.0, INF)), (list(range(16)), (0.0, INF), (1e5, 2e6)),
+              ([22, 5], (0.0, INF), (0.0, INF)), (list(range(20, 40)), (50.0, 5e5), (0.0, 3e6))]
+    wy, wo = oracle.ylt_olt(C, yet, None, N, K, elts, layers)
+    ctx = _ctx_from(C, elts, layers)
+    ids = torch.from_numpy(yet.view(np.int32)).cuda()
+    for k in (ara.KERNEL_AUTO, ara.KERNEL_PRESENCE, ara.KERNEL_DENSE):
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
+        y = torch.zeros((len(layers), N), dtype=torch.float64, device=cuda_device)
+        o = torch.zeros((len(layers), N), dtype=torch.float64, device=cuda_device)
+        ctx.ara_run_ex(ids, y, o, events_per_trial=K, num_trials=N)
+        ctx.ara_check()
+        assert np.array_equal(y.cpu().numpy(), wy) and np.array_equal(o.cpu().numpy(), wo), k
+
+
+def test_host_path_multi_layer_and_unaligned_buffer(cuda_device):
+    C, elts, layer, yet, N, K = _small_problem(16, seed=21, N=500, K=99)
+    layers = [layer, (list(range(8)), (0.0, INF), (0.0, INF))]
+    want = oracle.ylt(C, yet, None, N, K, elts, layers)
+    ctx = _ctx_from(C, elts, layers)
+    out = np.zeros((2, N))
+    ctx.ara_run_host(yet, out, events_per_trial=K, num_trials=N)
+    assert np.array_equal(out, want)
+    # a device YET starting 4 bytes past an allocation (not 16-B aligned): scalar loads
+    padded = torch.from_numpy(np.concatenate([np.zeros(1, np.uint32), yet]).view(np.int32)).cuda()
+    y = torch.zeros((2, N), dtype=torch.float64, device=cuda_device)
+    ctx.ara_run(padded[1:], y, events_per_trial=K, num_trials=N)
+    ctx.ara_check()
+    assert np.array_equal(y.cpu().numpy(), want)
