@@ -145,6 +145,11 @@ ARA_API ara_status ara_check(ara_ctx* ctx, void* stream);
  * (1, n] or not finite), ARA_E_NOMEM, ARA_E_CUDA. */
 ARA_API ara_status ara_pml_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_out,
                         double* tvar_out, void* stream);
+/* Asynchronous form: results to DEVICE pml_dev[m] / tvar_dev[m] (either may be NULL), enqueued on
+ * `stream` without synchronising, so successive analyses pipeline without host round trips.
+ * ARA_E_UNSUPPORTED if the device refuses the cooperative launch the fused kernel needs. */
+ARA_API ara_status ara_pml_tvar_device(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
+                                       double* tvar_dev, void* stream);
 ARA_API ara_status ara_pml(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream);
 ARA_API ara_status ara_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream);
 

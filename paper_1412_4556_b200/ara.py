@@ -29,7 +29,7 @@ ARA_MAX_ELTS_PER_LAYER = 128
 #: every symbol include/ara.h declares (checked by tests/test_abi.py against the header and the .so)
 EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_ex", "ara_run_host", "ara_run_study", "ara_aal", "ara_ep",
            "ara_sum_layers", "ara_check", "ara_pml_tvar", "ara_pml",
-           "ara_tvar", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
+           "ara_tvar", "ara_pml_tvar_device", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
            "ara_layer_info", "ara_layer_stats", "ara_table_row", "ara_status_string", "ara_last_error", "ara_version")
 
 
@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
             "ara_check": (st, [vp, vp]),
             "ara_pml_tvar": (st, [dp, u64, dp, u32, dp, dp, vp]),
             "ara_pml": (st, [dp, u64, dp, u32, dp, vp]),
+            "ara_pml_tvar_device": (st, [dp, u64, dp, u32, dp, dp, vp]),
             "ara_tvar": (st, [dp, u64, dp, u32, dp, vp]),
             "ara_table_footprint": (st, [u32, u32, ctypes.POINTER(u64), ctypes.POINTER(u32)]),
             "ara_unshard": (st, [dp, u32, u64, u32, dp, dp, vp]),
@@ -302,6 +303,14 @@ def ara_pml_tvar(ylt, rps: Sequence[float], stream=None, n: Optional[int] = None
     _check(lib().ara_pml_tvar(_dptr(ylt), n, _dptr(r), r.size, _dptr(pml), _dptr(tv), _stream_ptr(stream)),
            "ara_pml_tvar")
     return pml[:r.size], tv[:r.size]
+
+
+def ara_pml_tvar_device(ylt, rps: Sequence[float], pml_dev, tvar_dev, stream=None, n: Optional[int] = None) -> None:
+    """Asynchronous PML/TVaR into CUDA float64 tensors pml_dev / tvar_dev (len(rps) each, either None)."""
+    r = np.ascontiguousarray(rps, dtype=np.float64)
+    n = _numel(ylt) if n is None else n
+    _check(lib().ara_pml_tvar_device(_dptr(ylt), n, _dptr(r), r.size, _dptr(pml_dev), _dptr(tvar_dev),
+                                     _stream_ptr(stream)), "ara_pml_tvar_device")
 
 
 def ara_pml(ylt, rps: Sequence[float], stream=None) -> np.ndarray:

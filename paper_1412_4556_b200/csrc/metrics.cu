@@ -234,9 +234,12 @@ __global__ void __launch_bounds__(kSelBlock) tail_pass(const double* __restrict_
 constexpr int kFusedBlock = 256;
 constexpr int kCacheKeys = 4096;  // 32 KB of cached keys per block
 
-struct FusedState {
+struct FusedState {  // zeroed (cudaMemsetAsync) before every launch
   unsigned int H[3][kMaxQ][256];
   unsigned int bar_count, bar_gen;
+};
+
+struct FusedQueries {  // kernel parameter
   uint64_t k[kMaxQ];
 };
 
@@ -261,7 +264,8 @@ __device__ __forceinline__ void grid_sync(unsigned int* count, unsigned int* gen
 __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __restrict__ y, uint64_t n, int m,
                                                               FusedState* st, double* __restrict__ psum,
                                                               unsigned long long* __restrict__ pcnt,
-                                                              double* __restrict__ out) {
+                                                              const __grid_constant__ FusedQueries Q,
+                                                              double* __restrict__ pml_out, double* __restrict__ tvar_out) {
   extern __shared__ uint64_t skeys[];
   __shared__ unsigned int sh[kMaxQ][256];
   __shared__ uint64_t s_prefix[kMaxQ], s_rank[kMaxQ], s_slot_prefix[kMaxQ];
@@ -278,7 +282,7 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) skeys[i] = to_key(y[lo + i]);
   if (threadIdx.x < m) {
     s_prefix[threadIdx.x] = 0;
-    s_rank[threadIdx.x] = st->k[threadIdx.x];
+    s_rank[threadIdx.x] = Q.k[threadIdx.x];
     s_q2slot[threadIdx.x] = 0;
   }
   if (threadIdx.x == 0) {
@@ -412,16 +416,18 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
       b += wcnt[i][q];
     }
     const double T = from_key(s_prefix[q]);
-    const uint64_t k = st->k[q];
-    out[q] = T;
-    out[kMaxQ + q] = __ddiv_rn(__dadd_rn(a, __dmul_rn((double)(k - b), T)), (double)k);
+    const uint64_t k = Q.k[q];
+    if (pml_out) pml_out[q] = T;  // PML: the k-th largest value
+    if (tvar_out) tvar_out[q] = __ddiv_rn(__dadd_rn(a, __dmul_rn((double)(k - b), T)), (double)k);  // TVaR
   }
 }
 
-// Launch the fused kernel cooperatively for one batch of <= kMaxQ queries; returns false if the
-// device refuses a cooperative launch of the needed size (caller falls back to the pass kernels).
+// Launch the fused kernel cooperatively for one batch of <= kMaxQ queries, results to DEVICE pml/tvar
+// (either may be null); asynchronous.  Returns false if the device refuses a cooperative launch of the
+// needed size (callers fall back to the pass kernels).
 static bool metrics_fused_batch(const double* ylt, uint64_t n, int mq, const uint64_t* ks, char* scratch,
-                                size_t scratch_bytes, double* h_out, cudaStream_t s, cudaError_t* err) {
+                                size_t scratch_bytes, double* pml_dev, double* tvar_dev, cudaStream_t s,
+                                cudaError_t* err) {
   int dev = 0, sms = 148, occ = 0;
   *err = cudaSuccess;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
@@ -440,23 +446,19 @@ static bool metrics_fused_batch(const double* ylt, uint64_t n, int mq, const uin
   const uint64_t need = (n + kFusedBlock - 1) / kFusedBlock;
   if (grid > need) grid = need;
   const size_t state = sizeof(FusedState);
-  const size_t need_bytes = state + grid * kMaxQ * (sizeof(double) + sizeof(unsigned long long)) + 2 * kMaxQ * sizeof(double);
+  const size_t need_bytes = state + grid * kMaxQ * (sizeof(double) + sizeof(unsigned long long));
   if (need_bytes > scratch_bytes) return false;
   FusedState* st = (FusedState*)scratch;
   double* psum = (double*)(scratch + state);
   unsigned long long* pcnt = (unsigned long long*)(psum + grid * kMaxQ);
-  double* d_out = (double*)(pcnt + grid * kMaxQ);
-  FusedState init;
-  memset(&init, 0, sizeof init);
-  for (int q = 0; q < mq; ++q) init.k[q] = ks[q];
-  if ((*err = cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s)) != cudaSuccess) return true;
+  FusedQueries Q;
+  memset(&Q, 0, sizeof Q);
+  for (int q = 0; q < mq; ++q) Q.k[q] = ks[q];
+  if ((*err = cudaMemsetAsync(st, 0, sizeof(FusedState), s)) != cudaSuccess) return true;
   int m_ = mq;
-  void* args[] = {(void*)&ylt, (void*)&n, (void*)&m_, (void*)&st, (void*)&psum, (void*)&pcnt, (void*)&d_out};
-  if ((*err = cudaLaunchCooperativeKernel((const void*)metrics_fused, dim3((unsigned)grid), dim3(kFusedBlock), args, dyn, s)) !=
-      cudaSuccess)
-    return true;
-  if ((*err = cudaMemcpyAsync(h_out, d_out, 2 * kMaxQ * sizeof(double), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return true;
-  *err = cudaStreamSynchronize(s);
+  void* args[] = {(void*)&ylt, (void*)&n, (void*)&m_, (void*)&st, (void*)&psum, (void*)&pcnt, (void*)&Q,
+                  (void*)&pml_dev, (void*)&tvar_dev};
+  *err = cudaLaunchCooperativeKernel((const void*)metrics_fused, dim3((unsigned)grid), dim3(kFusedBlock), args, dyn, s);
   return true;
 }
 
@@ -471,66 +473,68 @@ static uint64_t metric_rank(uint64_t n, double rp) {
   return (uint64_t)ceil(x - 1e-9 * x);
 }
 
-static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml, double* tvar,
-                          cudaStream_t s) {
-  const bool use_fused = getenv("ARA_METRICS_PASSES") == nullptr;  // env switch keeps the pass kernels testable
-  if (!ylt || !rps || n == 0 || m == 0 || m > ARA_MAX_RETURN_PERIODS)
-    return set_error(ARA_E_ARG, "invalid metric arguments");
-  std::vector<uint64_t> ks(m);
+static ara_status ranks_for(uint64_t n, const double* rps, uint32_t m, std::vector<uint64_t>& ks) {
+  if (!rps || n == 0 || m == 0 || m > ARA_MAX_RETURN_PERIODS) return set_error(ARA_E_ARG, "invalid metric arguments");
+  ks.resize(m);
   for (uint32_t i = 0; i < m; ++i) {
     ks[i] = metric_rank(n, rps[i]);
     if (!ks[i]) return set_error(ARA_E_RANGE, "return period %g outside (1, %llu]", rps[i], (unsigned long long)n);
   }
+  return ARA_OK;
+}
+
+// Scratch: [2*kMaxQ doubles of batch results][state][block partials].
+static size_t scratch_bytes(uint64_t n, uint64_t* blocks_out) {
   int dev = 0, sms = 148;
-  ARA_CUDA(cudaGetDevice(&dev));
-  ARA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   uint64_t blocks = (n + kSelBlock - 1) / kSelBlock;
   if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;  // covers the fused grid (<= SMs x occupancy)
-  SelState* st = nullptr;
-  double* psum = nullptr;
-  unsigned long long* pcnt = nullptr;
-  double* d_out = nullptr;
-  const size_t bytes = std::max(sizeof(SelState), sizeof(FusedState)) +
-                       blocks * kMaxQ * (sizeof(double) + sizeof(unsigned long long)) + 2 * kMaxQ * sizeof(double);
+  *blocks_out = blocks;
+  return 2 * kMaxQ * sizeof(double) + std::max(sizeof(SelState), sizeof(FusedState)) +
+         blocks * kMaxQ * (sizeof(double) + sizeof(unsigned long long));
+}
+
+static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml, double* tvar,
+                          cudaStream_t s) {
+  const bool use_fused = getenv("ARA_METRICS_PASSES") == nullptr;  // env switch keeps the pass kernels testable
+  if (!ylt) return set_error(ARA_E_ARG, "ylt is NULL");
+  std::vector<uint64_t> ks;
+  ara_status rc = ranks_for(n, rps, m, ks);
+  if (rc) return rc;
+  uint64_t blocks = 0;
+  const size_t bytes = scratch_bytes(n, &blocks);
   char* scratch = nullptr;
   ARA_CUDA(cudaMallocAsync((void**)&scratch, bytes, s));
-  st = (SelState*)scratch;
-  psum = (double*)(scratch + sizeof(SelState));
-  pcnt = (unsigned long long*)(psum + blocks * kMaxQ);
-  d_out = (double*)(pcnt + blocks * kMaxQ);
+  double* d_out = (double*)scratch;
+  char* rest = scratch + 2 * kMaxQ * sizeof(double);
+  const size_t rest_bytes = bytes - 2 * kMaxQ * sizeof(double);
+  SelState* st = (SelState*)rest;
+  double* psum = (double*)(rest + std::max(sizeof(SelState), sizeof(FusedState)));
+  unsigned long long* pcnt = (unsigned long long*)(psum + blocks * kMaxQ);
   std::vector<double> h_out(2 * kMaxQ);
   SelState init;
-  ara_status rc = ARA_OK;
   for (uint32_t q0 = 0; q0 < m && rc == ARA_OK; q0 += kMaxQ) {
     const int mq = (int)std::min<uint32_t>(kMaxQ, m - q0);
-    memset(&init, 0, sizeof init);
-    for (int q = 0; q < mq; ++q) {
-      init.rank[q] = ks[q0 + q];
-      init.k[q] = ks[q0 + q];
-      init.q2slot[q] = 0;
-    }
-    init.nslot = 1;  // pass 0: every prefix is empty
-    init.slot_prefix[0] = 0;
     cudaError_t e = cudaSuccess;
-    if (use_fused && metrics_fused_batch(ylt, n, mq, &ks[q0], scratch, bytes, h_out.data(), s, &e)) {
-      if (e != cudaSuccess) {
-        rc = cuda_error(e, "fused metric kernel");
-        break;
-      }
+    if (!(use_fused && metrics_fused_batch(ylt, n, mq, &ks[q0], rest, rest_bytes, d_out, d_out + kMaxQ, s, &e))) {
+      memset(&init, 0, sizeof init);
       for (int q = 0; q < mq; ++q) {
-        if (pml) pml[q0 + q] = h_out[q];
-        if (tvar) tvar[q0 + q] = h_out[kMaxQ + q];
+        init.rank[q] = ks[q0 + q];
+        init.k[q] = ks[q0 + q];
+        init.q2slot[q] = 0;
       }
-      continue;
-    }
-    e = cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s);
-    for (int pass = 0; pass < 8 && e == cudaSuccess; ++pass) {
-      select_pass<<<(unsigned)blocks, kSelBlock, 0, s>>>(ylt, n, mq, pass, st);
-      e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) {
-      tail_pass<<<(unsigned)blocks, kSelBlock, 0, s>>>(ylt, n, mq, st, psum, pcnt, d_out);
-      e = cudaGetLastError();
+      init.nslot = 1;  // pass 0: every prefix is empty
+      init.slot_prefix[0] = 0;
+      e = cudaMemcpyAsync(st, &init, sizeof init, cudaMemcpyHostToDevice, s);
+      for (int pass = 0; pass < 8 && e == cudaSuccess; ++pass) {
+        select_pass<<<(unsigned)blocks, kSelBlock, 0, s>>>(ylt, n, mq, pass, st);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) {
+        tail_pass<<<(unsigned)blocks, kSelBlock, 0, s>>>(ylt, n, mq, st, psum, pcnt, d_out);
+        e = cudaGetLastError();
+      }
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.data(), d_out, 2 * kMaxQ * sizeof(double), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -547,6 +551,30 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
   return rc;
 }
 
+// Asynchronous variant: results to DEVICE pml_dev[m] / tvar_dev[m]; needs cooperative launch.
+static ara_status metrics_device(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
+                                 double* tvar_dev, cudaStream_t s) {
+  if (!ylt || (!pml_dev && !tvar_dev)) return set_error(ARA_E_ARG, "NULL argument");
+  std::vector<uint64_t> ks;
+  ara_status rc = ranks_for(n, rps, m, ks);
+  if (rc) return rc;
+  uint64_t blocks = 0;
+  const size_t bytes = scratch_bytes(n, &blocks);
+  char* scratch = nullptr;
+  ARA_CUDA(cudaMallocAsync((void**)&scratch, bytes, s));
+  for (uint32_t q0 = 0; q0 < m && rc == ARA_OK; q0 += kMaxQ) {
+    const int mq = (int)std::min<uint32_t>(kMaxQ, m - q0);
+    cudaError_t e = cudaSuccess;
+    if (!metrics_fused_batch(ylt, n, mq, &ks[q0], scratch, bytes, pml_dev ? pml_dev + q0 : nullptr,
+                             tvar_dev ? tvar_dev + q0 : nullptr, s, &e))
+      rc = set_error(ARA_E_UNSUPPORTED, "cooperative launch unavailable for the asynchronous metrics");
+    else if (e != cudaSuccess)
+      rc = cuda_error(e, "fused metric kernel");
+  }
+  cudaFreeAsync(scratch, s);
+  return rc;
+}
+
 }  // namespace ara
 
 extern "C" {
@@ -555,6 +583,11 @@ ara_status ara_pml_tvar(const double* ylt, uint64_t n, const double* rps, uint32
                         double* tvar_out, void* stream) {
   if (!pml_out && !tvar_out) return ara::set_error(ARA_E_ARG, "no output");
   return ara::metrics(ylt, n, rps, m, pml_out, tvar_out, (cudaStream_t)stream);
+}
+
+ara_status ara_pml_tvar_device(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
+                               double* tvar_dev, void* stream) {
+  return ara::metrics_device(ylt, n, rps, m, pml_dev, tvar_dev, (cudaStream_t)stream);
 }
 
 ara_status ara_pml(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* out, void* stream) {

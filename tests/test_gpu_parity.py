@@ -384,6 +384,34 @@ def test_metrics_fused_and_pass_kernels_agree(cuda_device, monkeypatch):
         assert np.array_equal(t1, oracle.tvar(y, rps)) and np.array_equal(t2, t1), n
 
 
+def test_metrics_device_outputs_async(cuda_device):
+    """ara_pml_tvar_device: results land in device buffers, enqueued back to back on one stream
+    (more than one 16-query batch, and one output omitted), equal to the oracle bitwise."""
+    rng = np.random.default_rng(5)
+    n = 500_000
+    ys = [np.floor(rng.exponential(1e6, n)) * (rng.random(n) > 0.4) for _ in range(3)]
+    rps = sorted(set([2.0, 3.0, 5.0, 10.0, 20.0, 25.0, 50.0, 100.0, 200.0, 250.0, 500.0, 1000.0, 2000.0,
+                      5000.0, 10000.0, 20000.0, 50000.0, 100000.0, 250000.0, 500000.0, 7.5]))
+    assert len(rps) > 16
+    s = torch.cuda.Stream()
+    ds = [torch.from_numpy(y).cuda() for y in ys]
+    torch.cuda.synchronize()
+    outs = []
+    with torch.cuda.stream(s):
+        for i, d in enumerate(ds):
+            p = torch.full((len(rps),), -1.0, dtype=torch.float64, device="cuda")
+            t = torch.full((len(rps),), -1.0, dtype=torch.float64, device="cuda") if i != 1 else None
+            ara.ara_pml_tvar_device(d, rps, p, t, stream=s)
+            outs.append((p, t))
+    s.synchronize()
+    for y, (p, t) in zip(ys, outs):
+        assert np.array_equal(p.cpu().numpy(), oracle.pml(y, rps))
+        if t is not None:
+            assert np.array_equal(t.cpu().numpy(), oracle.tvar(y, rps))
+    with pytest.raises(ara.AraError):
+        ara.ara_pml_tvar_device(ds[0], [n * 2.0], outs[0][0], None)
+
+
 @pytest.mark.parametrize("layout", [ara.STUDY_INTERLEAVED, ara.STUDY_INDEPENDENT, ara.STUDY_SORTED])
 def test_section_4b_study_layouts(cuda_device, layout):
     """The Section IV.B data-structure study kernels compute the same YLT."""
