@@ -63,7 +63,10 @@ struct Layer {
   uint32_t J = 0, jpad = 0;
   float* table = nullptr;
   uint64_t table_bytes = 0;
-  uint32_t* present = nullptr;  // presence bitmap, (C + 1 + 31) / 32 words
+  uint32_t* present = nullptr;  // presence bitmap, (C + 1 + 31) / 32 words: bit e set iff row e holds a loss
+  uint32_t* folded = nullptr;   // the bitmap folded for the presence kernel's shared memory (same size)
+  uint32_t folded_words = 0;    // words of the current fold (0: not built yet)
+  uint32_t fold_mul = 0;        // its multiplier (LayerParams::fold_mul)
   uint4* rec = nullptr;         // sparse row records (C + 1) x 16 B, rows of <= 16 columns
   // Section IV.B study structures, built on first use by ara_run_study
   float* indep = nullptr;         // J x (C + 1) independent per-ELT direct-access arrays
@@ -177,6 +180,24 @@ __global__ void __launch_bounds__(256) presence_build_kernel(uint32_t* __restric
 }
 
 
+// Fold the presence bitmap into `fw` words for the presence kernel: row e >= 1 (x = e - 1) sets bit
+// x & 31 of word umulhi(x, mul); x = C is the always-set sentinel that catches invalid ids.
+__global__ void __launch_bounds__(256) presence_fold_kernel(uint32_t* __restrict__ folded,
+                                                            const uint32_t* __restrict__ present, uint32_t words,
+                                                            uint32_t C, uint32_t mul) {
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    uint32_t v = present[w];
+    while (v) {
+      const uint32_t e = w * 32u + (uint32_t)(__ffs(v) - 1);
+      v &= v - 1u;
+      if (e == 0u || e > C) continue;
+      const uint32_t x = e - 1u;
+      atomicOr(folded + __umulhi(x, mul), 1u << (x & 31u));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(folded + __umulhi(C, mul), 1u << (C & 31u));
+}
+
 // Sparse record per table row (see ld_rec in ara_kernel.cuh): the first two non-zero columns and losses
 // and the count of non-zero columns.
 __global__ void __launch_bounds__(256) record_build_kernel(uint4* __restrict__ rec, const float* __restrict__ table,
@@ -207,6 +228,7 @@ static void destroy_ctx(ara_ctx* c) {
   for (auto& L : c->layers) {
     cudaFree(L.table);
     cudaFree(L.present);
+    cudaFree(L.folded);
     cudaFree(L.rec);
     cudaFree(L.indep);
     cudaFree(L.sorted_ids);
@@ -227,6 +249,13 @@ static void destroy_ctx(ara_ctx* c) {
   delete c;
 }
 
+// Dynamic shared memory of a presence variant besides the bitmap: the per-warp hit queues and, for
+// narrow rows (record batches), 32 x 16-B record slots per warp (+16 B alignment slack).
+static size_t presence_warp_smem(const Variant* v) {
+  const bool rec = v->G == 1 && v->V * v->NV <= 16;
+  return (size_t)v->NW * kQueue * 4 + (rec ? (size_t)v->NW * 512 + 16 : 0);
+}
+
 static int kind_of(const ara_ctx* c, const Layer& L) { return c->kernel < 0 ? L.auto_kind : c->kernel; }
 
 static const Variant* pick(const ara_ctx* c, const Layer& L) {
@@ -236,7 +265,7 @@ static const Variant* pick(const ara_ctx* c, const Layer& L) {
   return vs[v];
 }
 
-static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, const uint64_t* offsets,
+static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const uint64_t* offsets,
                                uint64_t num_trials, uint64_t num_events, uint32_t K, double* ylt, double* olt,
                                cudaStream_t stream) {
   if (num_trials == 0) return ARA_OK;
@@ -269,14 +298,25 @@ static ara_status launch_layer(ara_ctx* c, const Layer& L, const uint32_t* ids, 
     threads = var->NW * 32;
     cudaFuncAttributes fa;
     ARA_CUDA(cudaFuncGetAttributes(&fa, (const void*)var->fn));
-    const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)var->NW * kQueue * 4;
+    const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)presence_warp_smem(var);
     if (budget < 4096) return set_error(ARA_E_UNSUPPORTED, "no shared memory left for the presence bitmap");
-    p.present = L.present;
+    // fold the bitmap into the words that fit (rebuilt, stream-ordered, when the budget changes)
+    const uint32_t fw = (uint32_t)std::min<int64_t>(L.present_words, budget / 4);
+    const uint64_t C = c->C;
+    const uint32_t mul = (C + 1 <= 32ull * fw) ? (1u << 27) : (uint32_t)((((uint64_t)fw << 32) - 1) / C);
+    if (L.folded_words != fw || L.fold_mul != mul) {
+      ARA_CUDA(cudaMemsetAsync(L.folded, 0, (size_t)fw * 4, stream));
+      const unsigned fb = (unsigned)std::min<uint64_t>((L.present_words + 255) / 256, 4096);
+      presence_fold_kernel<<<fb, 256, 0, stream>>>(L.folded, L.present, L.present_words, c->C, mul);
+      ARA_CUDA(cudaGetLastError());
+      L.folded_words = fw;
+      L.fold_mul = mul;
+    }
+    p.present = L.folded;
     p.rec = L.rec;
-    p.present_words = L.present_words;
-    p.fold_words = (uint32_t)std::min<int64_t>(L.present_words, budget / 4);
-    p.fold_magic = UINT64_MAX / p.fold_words + 1;
-    dyn_smem = ((size_t)p.fold_words + (size_t)var->NW * kQueue) * 4;
+    p.present_words = fw;
+    p.fold_mul = mul;
+    dyn_smem = (size_t)fw * 4 + presence_warp_smem(var);
     ARA_CUDA(cudaFuncSetAttribute((const void*)var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
     ARA_CUDA(cudaFuncSetAttribute((const void*)var->fn_olt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
   }
@@ -434,7 +474,8 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
     }
     CK(cudaMemsetAsync(L.table, 0, L.table_bytes, s));
     L.present_words = (uint32_t)(((uint64_t)catalog_size + 1 + 31) / 32);
-    if (cudaMalloc(&L.present, (size_t)L.present_words * 4) != cudaSuccess) {
+    if (cudaMalloc(&L.present, (size_t)L.present_words * 4) != cudaSuccess ||
+        cudaMalloc(&L.folded, (size_t)L.present_words * 4) != cudaSuccess) {
       cudaGetLastError();
       FAIL(set_error(ARA_E_NOMEM, "presence bitmap for layer %u", l));
     }
@@ -449,7 +490,7 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       const Variant* pv = L.variants[KIND_PRESENCE][0];
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, (const void*)pv->fn));
-      const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)pv->NW * kQueue * 4;
+      const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)presence_warp_smem(pv);
       const double pw = (double)(((uint64_t)catalog_size + 1 + 31) / 32);
       const double fw = budget > 0 ? std::min(pw, (double)(budget / 4)) : 1.0;
       const double dens = (double)L.present_rows / ((double)catalog_size + 1.0);

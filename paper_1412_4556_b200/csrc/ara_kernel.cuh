@@ -42,10 +42,10 @@ struct LayerParams {
   double* olt;               // this layer's OLT row (largest occurrence-net loss per trial) or nullptr
   unsigned* err;             // bit0: id out of range, bit1: bad offsets
   double r2, l2, r3, l3;     // FT2, FT3
-  const uint32_t* present;   // presence bitmap: bit e set iff row e holds a non-zero loss (presence kernel)
-  uint32_t present_words;    // (C + 1 + 31) / 32
-  uint32_t fold_words;       // bitmap words held in shared memory (<= present_words; folded mod fold_words)
-  uint64_t fold_magic;       // floor((2^64 - 1) / fold_words) + 1: fast word % fold_words (Lemire)
+  const uint32_t* present;   // FOLDED presence bitmap (presence kernel): for x = e - 1, bit x & 31 of word
+                             // umulhi(x, fold_mul) is set if row e holds a non-zero loss; x = C: sentinel
+  uint32_t present_words;    // words of the folded bitmap (staged in shared memory)
+  uint32_t fold_mul;         // 2^27 (no folding: word x >> 5) or floor((present_words * 2^32 - 1) / C)
   const uint4* rec;          // per-event sparse row record (presence kernel, rows <= 16 columns)
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
@@ -159,6 +159,17 @@ __device__ __forceinline__ void sts_u32_if(uint32_t saddr, uint32_t v, bool pred
 __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
+// 16-byte asynchronous global -> shared copy (L2 only), completion awaited with cp_async_wait_all.
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(saddr), "l"(g), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ uint4 lds_u128(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr) : "memory");
   return v;
 }
 __device__ __forceinline__ unsigned lanemask_lt() {

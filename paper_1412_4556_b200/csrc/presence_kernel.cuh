@@ -42,9 +42,9 @@ struct RowBatch {
                                               unsigned head, int n, int lane, uint64_t pol_tab) {
     const int g = lane % G;
     const int slot = r * RG + lane / G;
-    // queue word = parity tag (bit 31) | event id; an id > C (invalid input that hit a folded bitmap
-    // word) fetches the zero row 0 instead
-    uint32_t id = slot < n ? (q[(head + slot) & (kQueue - 1)] & 0x7fffffffu) : 0u;
+    // queue word = event id; an invalid id (0 or > C, queued through the sentinel bit and reported by
+    // the kernel) fetches the zero row 0 instead
+    uint32_t id = slot < n ? q[(head + slot) & (kQueue - 1)] : 0u;
     id = id <= p.C ? id : 0u;
     const float* row = p.table + (uint64_t)id * (V * NV);
     float(&xr)[NVL][V] = x[kAsync ? r : 0];
@@ -130,29 +130,35 @@ struct RowBatch {
 // RECORD instead of its full row.  Typically a present row has a single non-zero loss (the ELTs are
 // sparse and nearly disjoint), so steps 1-3 cost two FT1 clamps and one FT2 clamp per row; a row with
 // more than two losses (rare) is read in full from the table.  The sum runs over the non-zero columns
-// in layer order, i.e. the oracle's order with its exact +0 terms dropped.
+// in layer order, i.e. the oracle's order with its exact +0 terms dropped.  The records travel by
+// cp.async into the warp's shared slots, so no registers are held while the warp scans on.
 template <int V, int NV>
 struct RecBatch {
   static constexpr bool kAsync = true;
-  uint4 r;
-  uint32_t id;
 
+  // lane -> slot `lane` of the warp's record buffer (rec_s: its 32-bit shared address)
   __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, unsigned head, int n,
-                                        int lane, uint64_t pol_tab) {
-    uint32_t e = lane < n ? (q[(head + lane) & (kQueue - 1)] & 0x7fffffffu) : 0u;
-    id = e <= p.C ? e : 0u;  // invalid ids (folded-bitmap collisions) read the zero record of row 0
-    r = ld_rec(p.rec + id, pol_tab);
+                                        int lane, uint64_t pol_tab, uint32_t rec_s) const {
+    const uint32_t e = lane < n ? q[(head + lane) & (kQueue - 1)] : 0u;
+    const uint32_t id = e <= p.C ? e : 0u;  // invalid ids (reported by the kernel) read the zero record of row 0
+    cp_async16(rec_s + 16u * (uint32_t)lane, p.rec + id, pol_tab);
+    cp_async_commit();
   }
 
-  // occurrence-net loss o = FT2(sum_j FT1(x_j)) of the lane's queued event
+  // occurrence-net loss o = FT2(sum_j FT1(x_j)) of the lane's queued event (queued at ring slot
+  // bhead + lane; the slot is not reused before the batch is consumed)
   __device__ __forceinline__ double row_loss(const LayerParams& p, const double* s_r1, const double* s_l1,
-                                             uint64_t pol_tab) const {
+                                             uint64_t pol_tab, uint32_t rec_s, const uint32_t* __restrict__ q,
+                                             unsigned bhead, int lane) const {
+    cp_async_wait_all();
+    const uint4 r = lds_u128(rec_s + 16u * (uint32_t)lane);
     const uint32_t c1 = r.x & 0xffu, c2 = (r.x >> 8) & 0xffu, nz = (r.x >> 16) & 0xffu;
     double sum = 0.0;
     if (__any_sync(0xffffffffu, nz > 2u)) {  // rare: some row of the batch has more than two losses
       if (nz > 2u) {
         constexpr int JP = V * NV;
-        const float* row = p.table + (uint64_t)id * JP;
+        const uint32_t e = q[(bhead + lane) & (kQueue - 1)];
+        const float* row = p.table + (uint64_t)(e <= p.C ? e : 0u) * JP;
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
           float x[V];
@@ -189,14 +195,27 @@ struct WarpTrials {
   uint32_t bad;
 };
 
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
+
 // V/NV: row format (as ara_layer_kernel); G: lanes per row in a batch; NW: warps per block.
 //
-// Hits are queued as (trial parity << 31 | event id) and, for narrow rows (G == 1), the queue is CARRIED
-// across the warp's consecutive trials: batches are always full (32 rows) except when the queue must be
-// flushed, so the per-trial partial batch disappears.  The occurrence-net loss of the i-th hit of a
-// trial is always accumulated by lane i mod 32 (a shuffle rotates each batch into that frame), and the
-// lanes are combined by the same xor-tree -- so a trial's fp64 summation order depends only on its own
-// ids, never on its neighbours, the sharding or the launch shape.
+// Presence test.  The shared bitmap is the layer's presence bitmap FOLDED to the words that fit: event
+// id e (x = e - 1) maps to bit x & 31 of word umulhi(x, fold_mul); fold_mul = 2^27 (no folding: word
+// x >> 5) or smaller, so neighbouring blocks of ids share words.  Folding only adds false positives
+// (gathers of all-zero rows, exact +0), never misses.  Any invalid id (0 or > C) clamps to x = C, whose
+// SENTINEL bit is always set, so invalid ids are queued like hits and reported when their batch is
+// issued: the scan itself needs no validity check.
+//
+// Hits are queued as raw event ids and, for narrow rows (G == 1), the queue is CARRIED across the warp's
+// consecutive trials: batches are always full (32 rows) except when the queue must be flushed, so the
+// per-trial partial batch disappears.  A queued hit's trial follows from its stream position (each open
+// trial owns [first, end)).  The occurrence-net loss of the i-th hit of a trial is always accumulated by
+// lane i mod 32 (a shuffle rotates each batch into that frame), and the lanes are combined by the same
+// xor-tree -- so a trial's fp64 summation order depends only on its own ids, never on its neighbours,
+// the sharding or the launch shape.
 // OLT: also track the largest occurrence-net loss per trial (ara_run_ex); a separate instantiation so
 // the plain YLT path carries no extra registers.
 template <int V, int NV, int G, int NW, bool OLT>
@@ -211,30 +230,21 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   constexpr int JPS = G * ((NV + G - 1) / G) * V;
   __shared__ double s_r1[JPS], s_l1[JPS];
   __shared__ WarpTrials s_wt[NW];
-  uint32_t* bits = smem;  // [fold_words]
+  uint32_t* bits = smem;  // [present_words], already folded by the host (fold_mul)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  uint32_t* q = smem + p.fold_words + warp * kQueue;
+  uint32_t* q = smem + p.present_words + warp * kQueue;
   WarpTrials& wt = s_wt[warp];
-  const uint32_t bits_s = (uint32_t)__cvta_generic_to_shared(bits);  // 32-bit shared addresses
-  const uint32_t q_s = (uint32_t)__cvta_generic_to_shared(q);
+  const uint32_t q_s = (uint32_t)__cvta_generic_to_shared(q);  // 32-bit shared addresses
+  // record slots (narrow rows): 32 x 16 B per warp after the queues, 16-B aligned
+  const uint32_t rec_s = (((uint32_t)__cvta_generic_to_shared(smem + p.present_words + NW * kQueue) + 15u) & ~15u) +
+                         (uint32_t)warp * 512u;
 
   for (int j = threadIdx.x; j < JPS; j += blockDim.x) {
     s_r1[j] = j < JP ? p.r1[j] : 0.0;
     s_l1[j] = j < JP ? p.l1[j] : __longlong_as_double(0x7ff0000000000000ll);
   }
-  // Stage the presence bitmap (folded modulo fold_words if it does not fit).
-  const uint32_t fw = p.fold_words;
-  if (p.present_words <= fw) {
-    for (uint32_t w = threadIdx.x; w < p.present_words; w += blockDim.x) bits[w] = __ldg(p.present + w);
-  } else {
-    for (uint32_t w = threadIdx.x; w < fw; w += blockDim.x) bits[w] = 0u;
-    __syncthreads();
-    for (uint32_t w = threadIdx.x; w < p.present_words; w += blockDim.x) {
-      const uint32_t v = __ldg(p.present + w);
-      if (v) atomicOr(&bits[w % fw], v);
-    }
-  }
+  for (uint32_t w = threadIdx.x; w < p.present_words; w += blockDim.x) bits[w] = __ldg(p.present + w);
   if (lane == 0) {
     wt.state[0] = wt.state[1] = 0u;
     wt.bad = 0u;
@@ -244,20 +254,19 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   const uint64_t pol_tab = make_policy(true, p.l2_hints);
   const uint64_t pol_yet = make_policy(false, p.l2_hints);
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(p.ids) & 15u) == 0);
-  const unsigned lt = (1u << lane) - 1u;
   const uint32_t C = p.C;
-  const bool fold_small = p.present_words <= 2u * fw;  // one conditional subtraction folds every word
-  const uint64_t fmagic = p.fold_magic;
-  const bool carry = kCarry && (C < 0x80000000u);      // the parity tag lives in bit 31 of a queue word
+  const uint32_t fmul = p.fold_mul;
+  const unsigned lt = lanemask_lt();
 
   double S0 = 0.0, S1 = 0.0;  // per-lane partial sums of the (<= 2) open trials, by parity
   double M0 = 0.0, M1 = 0.0;  // per-lane largest occurrence-net loss of those trials (OLT)
   constexpr bool want_olt = OLT;
-  unsigned head = 0, count = 0;  // ring of queued, not yet issued hits
-  uint32_t issued = 0;           // stream position of the next hit to issue
+  unsigned count = 0;            // queued, not yet issued hits (ring slots issued .. issued + count - 1)
+  uint32_t issued = 0;           // stream position of the next hit to issue (ring slot: issued mod kQueue)
   Batch rows;
-  uint32_t bstart = 0, btag = 0; // pending batch: stream position of slot 0; this lane's entry tag
+  uint32_t bstart = 0;           // pending batch: stream position of slot 0
   int bn = 0;                    // pending batch size (0 = none)
+  unsigned bad = 0;
 
   // FT3 on the warp-combined sum of parity slot a; lane 0 writes the YLT.
   auto finalize = [&](int a) {
@@ -292,24 +301,29 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   auto consume = [&]() {
     if (bn != 0) {
       if constexpr (kCarry) {
-        const double o = rows.row_loss(p, s_r1, s_l1, pol_tab);
-        const bool mine = lane < bn;
-        if (want_olt && mine) {  // the maximum needs no canonical order: the source lane keeps it
-          if (btag) M1 = o > M1 ? o : M1;
-          else M0 = o > M0 ? o : M0;
-        }
+        const double o = rows.row_loss(p, s_r1, s_l1, pol_tab, rec_s, q, bstart & (kQueue - 1), lane);
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
           if (wt.state[a] == 0u) continue;  // warp-uniform
-          const int src = (int)((uint32_t)lane + wt.first[a] - bstart) & 31;
-          const double oa = __shfl_sync(FULL, o, src);
-          const bool ok = __shfl_sync(FULL, mine && btag == (uint32_t)a, src);
-          if (ok) {
+          // this lane accumulates the trial's hit number (lane mod 32): batch slot src
+          const uint32_t src = ((uint32_t)lane + wt.first[a] - bstart) & 31u;
+          const double oa = __shfl_sync(FULL, o, (int)src);
+          const uint32_t rel = bstart + src - wt.first[a];  // position of that hit within trial a
+          // hits of trial a so far (all of them once scanned); batch positions are < issued
+          const uint32_t len_a = (wt.state[a] == 2u ? wt.end[a] : issued + count) - wt.first[a];
+          if (src < (uint32_t)bn && rel < len_a) {
             if (a) S1 += oa; else S0 += oa;
+          }
+          if (want_olt) {  // the maximum needs no canonical order: the source lane keeps it
+            const uint32_t relm = bstart + (uint32_t)lane - wt.first[a];
+            if (lane < bn && relm < len_a) {
+              if (a) M1 = o > M1 ? o : M1;
+              else M0 = o > M0 ? o : M0;
+            }
           }
         }
       } else {
-        if constexpr (!kCarry) rows.consume(p, lane, s_r1, s_l1, S0, M0);
+        rows.consume(p, lane, s_r1, s_l1, S0, M0);
       }
       bn = 0;
     }
@@ -319,18 +333,17 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   auto issue = [&](int n) {
     consume();
     __syncwarp();
-    const uint32_t word = lane < n ? q[(head + lane) & (kQueue - 1)] : 0u;
-    btag = word >> 31;
+    const uint32_t e = lane < n ? q[(issued + lane) & (kQueue - 1)] : 1u;
+    bad |= (e - 1u >= C) ? 1u : 0u;  // an invalid id reached the queue through the sentinel bit
     if constexpr (kCarry) {
-      rows.issue(p, q, head, n, lane, pol_tab);
+      rows.issue(p, q, issued, n, lane, pol_tab, rec_s);
     } else {
-      rows.issue(p, q, head, n, lane, pol_tab, s_r1, s_l1, S0, M0);
+      rows.issue(p, q, issued, n, lane, pol_tab, s_r1, s_l1, S0, M0);
     }
     __syncwarp();
     bstart = issued;
     bn = n;
     issued += (uint32_t)n;
-    head = (head + (unsigned)n) & (kQueue - 1);
     count -= (unsigned)n;
     if constexpr (!kCarry) consume();  // wide rows: rows.issue already consumed round by round
   };
@@ -338,9 +351,43 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     while (count > 0) issue(count < 32 ? (int)count : 32);
     consume();
   };
+  // Presence test of one id (see above): one VIADDMNMX, IMAD.HI, LDS, shift, and.
+  auto present = [&](uint32_t id) -> bool {
+    const uint32_t x = min(id - 1u, C);
+    return (bits[__umulhi(x, fmul)] >> (x & 31u)) & 1u;
+  };
+  // Scan one window: lane l holds window positions 4l .. 4l+3 (ids v); CHECKED windows mask positions
+  // outside the trial (r = window position of id 0 relative to the trial start, len = trial length).
+  auto scan = [&](const uint4 v, auto checked, uint32_t r, uint32_t len) {
+    const uint32_t id[4] = {v.x, v.y, v.z, v.w};
+    bool hit[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      hit[u] = present(id[u]);
+      if constexpr (decltype(checked)::value) hit[u] = hit[u] && (r + (uint32_t)u < len);
+    }
+    // Append the hits in a fixed order that depends only on the window: per pair of slots, first the
+    // lanes' first hit of the pair (lanes ascending), then -- only if some lane hit both -- the
+    // second ids of those lanes.  One ballot per pair instead of one per slot.
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const bool ha = hit[2 * h], hb = hit[2 * h + 1];
+      const bool any = ha || hb;
+      const uint32_t first = ha ? id[2 * h] : id[2 * h + 1];
+      const unsigned m = ballot_full(any);
+      sts_u32_if(q_s + 4u * ((issued + count + __popc(m & lt)) & (kQueue - 1)), first, any);
+      count += __popc(m);
+      const bool both = ha && hb;
+      if (any_full(both)) {  // rare: ~1% of lanes per pair
+        const unsigned m2 = ballot_full(both);
+        sts_u32_if(q_s + 4u * ((issued + count + __popc(m2 & lt)) & (kQueue - 1)), id[2 * h + 1], both);
+        count += __popc(m2);
+      }
+      while (count >= 32) issue(32);  // warp-uniform; at most 31 + 64 = 95 < kQueue queued
+    }
+  };
 
-  unsigned bad = 0;
-  uint32_t k = 0;    // local trial counter (parity = k & 1)
+  uint32_t k = 0;  // local trial counter (parity = k & 1)
   for (uint64_t t = (uint64_t)blockIdx.x * NW + warp; t < p.num_trials; t += (uint64_t)gridDim.x * NW, ++k) {
     const int par = (int)(k & 1u);
     if (wt.state[par] != 0u) flush();  // trial k-2 still has hits in flight
@@ -351,7 +398,6 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       wt.state[par] = 1u;
     }
     __syncwarp();
-    const uint32_t tag = (uint32_t)par << 31;
 
     uint64_t b, e;
     if (p.offsets) {
@@ -366,87 +412,44 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       e = b + p.K;
     }
     const uint32_t len = (uint32_t)(e - b);
-    const uint32_t* base = p.ids + b;
-    // Windows of 128 ids from the trial's first occurrence; lane l holds ids [rel + 4l, rel + 4l + 4):
-    // one 16-B vector when the trial start is 16-B aligned, else scalar loads.  Ids past the end read 0.
+    // Windows of 128 ids from the trial's first occurrence (so the order in which a trial's hits are
+    // queued depends only on the trial itself): lane l holds window positions 4l .. 4l+3.  When the
+    // trial start is 16-B aligned, full windows are single 16-B vectors streamed through a running
+    // per-lane pointer with no checks, one window held ahead in registers; the last partial window (or
+    // an unaligned trial) goes through the checked loader.
     const bool vec = vec_ok && ((b & 3u) == 0);
-    auto load4 = [&](uint32_t rel) -> uint4 {
-      const uint32_t qq = rel + 4u * lane;
-      if (vec && rel + 128 <= len) return ld_ids4(base + qq, pol_yet);  // warp-uniform fast path
+    const uint32_t nwin = (len + 127u) / 128u;
+    const uint32_t wf1 = vec ? len / 128u : 0u;  // full windows
+    auto load_checked = [&](uint32_t w) -> uint4 {
+      const uint32_t r = w * 128u + 4u * lane;  // trial position of this lane's first slot
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (qq < len) {
-        if (vec && qq + 4 <= len) {
-          v = ld_ids4(base + qq, pol_yet);
-        } else {
-          v.x = ld_id(base + qq, pol_yet);
-          if (qq + 1 < len) v.y = ld_id(base + qq + 1, pol_yet);
-          if (qq + 2 < len) v.z = ld_id(base + qq + 2, pol_yet);
-          if (qq + 3 < len) v.w = ld_id(base + qq + 3, pol_yet);
-        }
-      }
+      if (vec && r + 4u <= len) return ld_ids4(p.ids + b + r, pol_yet);
+      if (r < len) v.x = ld_id(p.ids + b + r, pol_yet);
+      if (r + 1u < len) v.y = ld_id(p.ids + b + r + 1, pol_yet);
+      if (r + 2u < len) v.z = ld_id(p.ids + b + r + 2, pol_yet);
+      if (r + 3u < len) v.w = ld_id(p.ids + b + r + 3, pol_yet);
       return v;
     };
-    // Full windows (16-B aligned trial, 128 ids inside the trial) stream through a running per-lane
-    // pointer with no bounds checks; the trial's last partial window (or an unaligned trial) goes
-    // through the checked loader.  One window is held ahead in registers (an extra L2 prefetch of
-    // windows further ahead measured slower).
-    const uint32_t nwin = (len + 127) / 128;
-    const uint32_t nfull = vec ? len / 128 : 0u;
-    const uint4* lp = reinterpret_cast<const uint4*>(base) + lane;
-    auto load_win = [&](uint32_t w) -> uint4 {
-      if (w < nfull) return ld_ids4(reinterpret_cast<const uint32_t*>(lp + (size_t)w * 32), pol_yet);
-      if (w < nwin) return load4(w * 128);
-      return make_uint4(0u, 0u, 0u, 0u);
-    };
-    uint32_t mxv = 0u, mnv = 0xffffffffu;  // extremes of the ids of the full windows
-    uint4 cur = load_win(0);
-    for (uint32_t w = 0; w < nwin; ++w) {
-      const uint4 nxt = load_win(w + 1);
-      const uint32_t id[4] = {cur.x, cur.y, cur.z, cur.w};
-      if (w < nfull) {  // validity is checked once per trial from the running extremes
-        mxv = max(mxv, max(max(id[0], id[1]), max(id[2], id[3])));
-        mnv = min(mnv, min(min(id[0], id[1]), min(id[2], id[3])));
-      } else {  // checked window: positions past the end read 0 and are excused
-        const uint32_t rel = w * 128;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) bad |= (rel + 4u * lane + u < len && id[u] - 1u >= C) ? 1u : 0u;
+    auto rel0 = [&](uint32_t w) -> uint32_t { return w * 128u + 4u * (uint32_t)lane; };
+    uint32_t w = 0;
+    if (w < wf1) {
+      const uint4* lp = reinterpret_cast<const uint4*>(p.ids + b) + lane;
+      uint4 cur = ld_ids4(reinterpret_cast<const uint32_t*>(lp + (size_t)w * 32), pol_yet);
+      for (; w < wf1; ++w) {
+        uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
+        if (w + 1 < wf1) nxt = ld_ids4(reinterpret_cast<const uint32_t*>(lp + (size_t)(w + 1) * 32), pol_yet);
+        scan(cur, BoolC<false>{}, 0u, 0u);
+        cur = nxt;
       }
-      bool hit[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint32_t wd = min(id[u], C) >> 5;  // an invalid id > C is clamped into the bitmap
-        wd = fold_small ? min(wd, wd - fw) : (uint32_t)__umul64hi(fmagic * (uint64_t)wd, (uint64_t)fw);
-        hit[u] = (lds_u32(bits_s + 4u * wd) >> (id[u] & 31u)) & 1u;  // id 0 -> bit 0 of word 0, never set
-      }
-      // Append the hits in a fixed order that depends only on the window: per pair of slots, first the
-      // lanes' first hit of the pair (lanes ascending), then -- only if some lane hit both -- the
-      // second ids of those lanes.  One ballot per pair instead of one per slot.
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const bool ha = hit[2 * h], hb = hit[2 * h + 1];
-        const bool any = ha || hb;
-        const uint32_t first = tag | (ha ? id[2 * h] : id[2 * h + 1]);
-        const unsigned m = __ballot_sync(FULL, any);
-        sts_u32_if(q_s + 4u * ((head + count + __popc(m & lanemask_lt())) & (kQueue - 1)), first, any);
-        count += __popc(m);
-        const bool both = ha && hb;
-        if (__any_sync(FULL, both)) {  // rare: ~1% of lanes per pair
-          const unsigned m2 = __ballot_sync(FULL, both);
-          sts_u32_if(q_s + 4u * ((head + count + __popc(m2 & lanemask_lt())) & (kQueue - 1)), tag | id[2 * h + 1], both);
-          count += __popc(m2);
-        }
-        while (count >= 32) issue(32);  // warp-uniform; at most 31 + 64 = 95 < kQueue queued
-      }
-      cur = nxt;
     }
-    if (nfull) bad |= (mnv == 0u || mxv > C) ? 1u : 0u;
+    for (; w < nwin; ++w) scan(load_checked(w), BoolC<true>{}, rel0(w), len);  // tail (or unaligned trial)
     __syncwarp();
     if (lane == 0) {
       wt.end[par] = issued + count;
       wt.state[par] = 2u;
     }
     __syncwarp();
-    if (!carry) {
+    if (!kCarry) {
       flush();  // wide rows: one trial at a time (finalized by the flush's settle)
     } else if (bn == 0) {
       settle(issued);  // nothing pending: a trial with no outstanding hits is final now
