@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(256) presence_fold_kernel(uint32_t* __restrict
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(folded + __umulhi(C, mul), 1u << (C & 31u));
 }
 
-// Sparse record per table row (see ld_rec in ara_kernel.cuh): the first two non-zero columns and losses
-// and the count of non-zero columns.
+// Sparse record per table row (see ld_rec in ara_kernel.cuh): the first two non-zero columns and losses,
+// the count of non-zero columns and the event id itself.
 __global__ void __launch_bounds__(256) record_build_kernel(uint4* __restrict__ rec, const float* __restrict__ table,
                                                            uint32_t jpad, uint64_t rows) {
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows; e += (uint64_t)gridDim.x * blockDim.x) {
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) record_build_kernel(uint4* __restrict__ r
       }
       ++n;
     }
-    rec[e] = make_uint4(c1 | (c2 << 8) | (n << 16), l1, l2, 0u);
+    rec[e] = make_uint4(c1 | (c2 << 8) | (n << 16), l1, l2, (uint32_t)e);
   }
 }
 

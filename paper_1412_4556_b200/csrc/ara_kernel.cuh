@@ -53,6 +53,7 @@ struct LayerParams {
 // Sparse record of one table row (built by ara_create for rows of <= 16 columns):
 //   x = c1 | c2 << 8 | n << 16   (n = non-zero losses in the row; c1 < c2 their columns, layer order)
 //   y = bits of the loss in column c1 (0 if n == 0), z = bits of the loss in column c2 (0 if n < 2)
+//   w = the event id (row index)
 // A row with n > 2 is read in full from the table.
 __device__ __forceinline__ uint4 ld_rec(const uint4* p, uint64_t pol) {
   uint4 v;

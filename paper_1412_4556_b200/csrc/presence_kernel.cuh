@@ -22,7 +22,7 @@
 
 namespace ara {
 
-constexpr int kQueue = 128;  // per-warp ring of pending hits (< 32 carried + <= 64 new per slot pair)
+constexpr int kQueue = 160;  // per-warp queue of pending hits (<= 31 left over + <= 128 new per window)
 
 // Gathers for a batch of up to 32 queued events, split into an ISSUE step (loads into registers)
 // and a CONSUME step (FT1 / sum / FT2 / accumulate), so a batch's L2 latency overlaps the scan of the
@@ -39,12 +39,12 @@ struct RowBatch {
   float x[R][NVL][V];
 
   __device__ __forceinline__ void issue_round(int r, const LayerParams& p, const uint32_t* __restrict__ q,
-                                              unsigned head, int n, int lane, uint64_t pol_tab) {
+                                              int n, int lane, uint64_t pol_tab) {
     const int g = lane % G;
     const int slot = r * RG + lane / G;
     // queue word = event id; an invalid id (0 or > C, queued through the sentinel bit and reported by
     // the kernel) fetches the zero row 0 instead
-    uint32_t id = slot < n ? q[(head + slot) & (kQueue - 1)] : 0u;
+    uint32_t id = slot < n ? q[slot] : 0u;
     id = id <= p.C ? id : 0u;
     const float* row = p.table + (uint64_t)id * (V * NV);
     float(&xr)[NVL][V] = x[kAsync ? r : 0];
@@ -99,13 +99,13 @@ struct RowBatch {
   }
 
   // Async: issue all rounds now, consume later.  Sync: issue+consume round by round.
-  __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, unsigned head, int n,
-                                        int lane, uint64_t pol_tab, const double* s_r1, const double* s_l1,
-                                        double& S, double& M) {
+  __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, int n, int lane,
+                                        uint64_t pol_tab, const double* s_r1, const double* s_l1, double& S,
+                                        double& M) {
 #pragma unroll
     for (int r = 0; r < G; ++r) {
       if (r * RG >= n) break;  // warp-uniform
-      issue_round(r, p, q, head, n, lane, pol_tab);
+      issue_round(r, p, q, n, lane, pol_tab);
       if constexpr (!kAsync) consume_round(r, p, lane, s_r1, s_l1, S, M);
     }
     if constexpr (kAsync) {
@@ -137,19 +137,17 @@ struct RecBatch {
   static constexpr bool kAsync = true;
 
   // lane -> slot `lane` of the warp's record buffer (rec_s: its 32-bit shared address)
-  __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, unsigned head, int n,
-                                        int lane, uint64_t pol_tab, uint32_t rec_s) const {
-    const uint32_t e = lane < n ? q[(head + lane) & (kQueue - 1)] : 0u;
+  __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, int n, int lane,
+                                        uint64_t pol_tab, uint32_t rec_s) const {
+    const uint32_t e = lane < n ? q[lane] : 0u;
     const uint32_t id = e <= p.C ? e : 0u;  // invalid ids (reported by the kernel) read the zero record of row 0
     cp_async16(rec_s + 16u * (uint32_t)lane, p.rec + id, pol_tab);
     cp_async_commit();
   }
 
-  // occurrence-net loss o = FT2(sum_j FT1(x_j)) of the lane's queued event (queued at ring slot
-  // bhead + lane; the slot is not reused before the batch is consumed)
+  // occurrence-net loss o = FT2(sum_j FT1(x_j)) of the lane's queued event
   __device__ __forceinline__ double row_loss(const LayerParams& p, const double* s_r1, const double* s_l1,
-                                             uint64_t pol_tab, uint32_t rec_s, const uint32_t* __restrict__ q,
-                                             unsigned bhead, int lane) const {
+                                             uint64_t pol_tab, uint32_t rec_s, int lane) const {
     cp_async_wait_all();
     const uint4 r = lds_u128(rec_s + 16u * (uint32_t)lane);
     const uint32_t c1 = r.x & 0xffu, c2 = (r.x >> 8) & 0xffu, nz = (r.x >> 16) & 0xffu;
@@ -157,8 +155,7 @@ struct RecBatch {
     if (__any_sync(0xffffffffu, nz > 2u)) {  // rare: some row of the batch has more than two losses
       if (nz > 2u) {
         constexpr int JP = V * NV;
-        const uint32_t e = q[(bhead + lane) & (kQueue - 1)];
-        const float* row = p.table + (uint64_t)(e <= p.C ? e : 0u) * JP;
+        const float* row = p.table + (uint64_t)r.w * JP;  // r.w: the record's own event id
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
           float x[V];
@@ -261,8 +258,10 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   double S0 = 0.0, S1 = 0.0;  // per-lane partial sums of the (<= 2) open trials, by parity
   double M0 = 0.0, M1 = 0.0;  // per-lane largest occurrence-net loss of those trials (OLT)
   constexpr bool want_olt = OLT;
-  unsigned count = 0;            // queued, not yet issued hits (ring slots issued .. issued + count - 1)
-  uint32_t issued = 0;           // stream position of the next hit to issue (ring slot: issued mod kQueue)
+  // The warp's queue is linear: the unissued hits are q[0 .. count), qt = q_s + 4 * count is the shared
+  // address of the next free slot; issuing a batch takes q[0 .. n) and moves the rest down.
+  uint32_t qt = q_s;
+  uint32_t issued = 0;           // stream position of the next hit to issue
   Batch rows;
   uint32_t bstart = 0;           // pending batch: stream position of slot 0
   int bn = 0;                    // pending batch size (0 = none)
@@ -301,7 +300,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   auto consume = [&]() {
     if (bn != 0) {
       if constexpr (kCarry) {
-        const double o = rows.row_loss(p, s_r1, s_l1, pol_tab, rec_s, q, bstart & (kQueue - 1), lane);
+        const double o = rows.row_loss(p, s_r1, s_l1, pol_tab, rec_s, lane);
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
           if (wt.state[a] == 0u) continue;  // warp-uniform
@@ -310,7 +309,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
           const double oa = __shfl_sync(FULL, o, (int)src);
           const uint32_t rel = bstart + src - wt.first[a];  // position of that hit within trial a
           // hits of trial a so far (all of them once scanned); batch positions are < issued
-          const uint32_t len_a = (wt.state[a] == 2u ? wt.end[a] : issued + count) - wt.first[a];
+          const uint32_t len_a = (wt.state[a] == 2u ? wt.end[a] : issued + ((qt - q_s) >> 2)) - wt.first[a];
           if (src < (uint32_t)bn && rel < len_a) {
             if (a) S1 += oa; else S0 += oa;
           }
@@ -333,22 +332,28 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   auto issue = [&](int n) {
     consume();
     __syncwarp();
-    const uint32_t e = lane < n ? q[(issued + lane) & (kQueue - 1)] : 1u;
+    const uint32_t count = (qt - q_s) >> 2;
+    const uint32_t e = lane < n ? q[lane] : 1u;
     bad |= (e - 1u >= C) ? 1u : 0u;  // an invalid id reached the queue through the sentinel bit
     if constexpr (kCarry) {
-      rows.issue(p, q, issued, n, lane, pol_tab, rec_s);
+      rows.issue(p, q, n, lane, pol_tab, rec_s);
     } else {
-      rows.issue(p, q, issued, n, lane, pol_tab, s_r1, s_l1, S0, M0);
+      rows.issue(p, q, n, lane, pol_tab, s_r1, s_l1, S0, M0);
     }
+    __syncwarp();  // every lane has read its batch slots
+    for (uint32_t i = (uint32_t)lane; i + (uint32_t)n < count; i += 32u) q[i] = q[i + n];  // n == 32 here
     __syncwarp();
     bstart = issued;
     bn = n;
     issued += (uint32_t)n;
-    count -= (unsigned)n;
+    qt -= 4u * (uint32_t)n;
     if constexpr (!kCarry) consume();  // wide rows: rows.issue already consumed round by round
   };
   auto flush = [&]() {
-    while (count > 0) issue(count < 32 ? (int)count : 32);
+    while (qt != q_s) {
+      const uint32_t count = (qt - q_s) >> 2;
+      issue(count < 32 ? (int)count : 32);
+    }
     consume();
   };
   // Presence test of one id (see above): one VIADDMNMX, IMAD.HI, LDS, shift, and.
@@ -375,16 +380,17 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       const bool any = ha || hb;
       const uint32_t first = ha ? id[2 * h] : id[2 * h + 1];
       const unsigned m = ballot_full(any);
-      sts_u32_if(q_s + 4u * ((issued + count + __popc(m & lt)) & (kQueue - 1)), first, any);
-      count += __popc(m);
+      sts_u32_if(qt + 4u * __popc(m & lt), first, any);
+      qt += 4u * __popc(m);
       const bool both = ha && hb;
       if (any_full(both)) {  // rare: ~1% of lanes per pair
         const unsigned m2 = ballot_full(both);
-        sts_u32_if(q_s + 4u * ((issued + count + __popc(m2 & lt)) & (kQueue - 1)), id[2 * h + 1], both);
-        count += __popc(m2);
+        sts_u32_if(qt + 4u * __popc(m2 & lt), id[2 * h + 1], both);
+        qt += 4u * __popc(m2);
       }
-      while (count >= 32) issue(32);  // warp-uniform; at most 31 + 64 = 95 < kQueue queued
     }
+    // warp-uniform; at most 31 + 128 = 159 < kQueue queued
+    while (qt - q_s >= 128u) issue(32);
   };
 
   uint32_t k = 0;  // local trial counter (parity = k & 1)
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     __syncwarp();
     if (lane == 0) {
       wt.trial[par] = t;
-      wt.first[par] = issued + count;  // stream position of the trial's first hit
+      wt.first[par] = issued + ((qt - q_s) >> 2);  // stream position of the trial's first hit
       wt.state[par] = 1u;
     }
     __syncwarp();
@@ -432,20 +438,23 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     };
     auto rel0 = [&](uint32_t w) -> uint32_t { return w * 128u + 4u * (uint32_t)lane; };
     uint32_t w = 0;
-    if (w < wf1) {
+    if (wf1 != 0u) {  // full windows: running pointer, one window held ahead
       const uint4* lp = reinterpret_cast<const uint4*>(p.ids + b) + lane;
-      uint4 cur = ld_ids4(reinterpret_cast<const uint32_t*>(lp + (size_t)w * 32), pol_yet);
-      for (; w < wf1; ++w) {
-        uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
-        if (w + 1 < wf1) nxt = ld_ids4(reinterpret_cast<const uint32_t*>(lp + (size_t)(w + 1) * 32), pol_yet);
+      uint4 cur = ld_ids4(reinterpret_cast<const uint32_t*>(lp), pol_yet);
+      for (uint32_t rem = wf1 - 1u;; --rem) {
+        lp += 32;
+        uint4 nxt;  // only read when rem != 0, i.e. when loaded
+        if (rem != 0u) nxt = ld_ids4(reinterpret_cast<const uint32_t*>(lp), pol_yet);
         scan(cur, BoolC<false>{}, 0u, 0u);
+        if (rem == 0u) break;
         cur = nxt;
       }
+      w = wf1;
     }
     for (; w < nwin; ++w) scan(load_checked(w), BoolC<true>{}, rel0(w), len);  // tail (or unaligned trial)
     __syncwarp();
     if (lane == 0) {
-      wt.end[par] = issued + count;
+      wt.end[par] = issued + ((qt - q_s) >> 2);
       wt.state[par] = 2u;
     }
     __syncwarp();
