@@ -70,33 +70,71 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md clocks line)."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled DURING the timed region (B200_PROFILING.md clocks line).
+
+    NVML is polled in-process every 5 ms from a thread started before the warm-up (so no tool start-up
+    lands inside the timed region); only samples between mark_start() and mark_end() are reported.
+    Falls back to `nvidia-smi -lms 10` when NVML is unavailable."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []  # (time, sm_mhz, max_mhz, reasons bitmask or names)
+        self.t0 = self.t1 = None
+        self.stop = threading.Event()
         self.proc = None
+        self.nvml = None
 
-    def __enter__(self):
+    def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "20", "-i", str(self.index)], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml = pynvml
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((time.perf_counter(), float(sm), float(mx), int(rs)))
+                    except Exception:  # noqa: BLE001
+                        pass
+                    self.stop.wait(0.005)
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
         except Exception:  # noqa: BLE001
-            self.proc = None
+            self.nvml = None
+            try:
+                q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                     "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+                self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                              "-lms", "10", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                             stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except Exception:  # noqa: BLE001
+                self.proc = None
         return self
 
     def _read(self):
+        names = list(self.REASONS)
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                bits = sum(self.REASONS[n] for n, v in zip(names, parts[2:]) if v.lower() == "active")
+                self.rows.append((time.perf_counter(), float(parts[0]), float(parts[1]), bits))
 
-    def __exit__(self, *a):
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
+
+    def close(self):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -105,14 +143,15 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        inside = [r for r in self.rows if self.t0 is not None and self.t1 is not None and self.t0 <= r[0] <= self.t1]
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        bits = 0
+        for r in inside:
+            bits |= r[3]
+        return {"sm_mhz": float(np.median([r[1] for r in inside])), "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": sorted(n for n, b in self.REASONS.items() if bits & b), "samples": len(inside),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def dist_env():
@@ -290,6 +329,7 @@ def main():
                          f"(0 of {got.size} outside tolerance)",
                "parity_checked": int(got.size)}
 
+    clk = ClockSampler(dev.index).start()  # started before the warm-up: no tool start-up inside the timed region
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -300,12 +340,14 @@ def main():
     # ---- timed region (warm: the table stays L2-resident; the 4 GB YET streams from HBM)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
-        start.record(stream)
-        for i in range(args.steps):
-            step(kev[i])
-        end.record(stream)
-        torch.cuda.synchronize()
+    clk.mark_start()
+    start.record(stream)
+    for i in range(args.steps):
+        step(kev[i])
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk.mark_end()
+    clk.close()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

@@ -166,6 +166,10 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(saddr), "l"(g), "l"(pol) : "memory");
 }
+// Bulk L2 prefetch of `bytes` (multiple of 16) from a 16-B aligned global address (one TMA request).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* g, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(g), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ uint4 lds_u128(uint32_t saddr) {

@@ -270,6 +270,9 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   // FT3 on the warp-combined sum of parity slot a; lane 0 writes the YLT.
   auto finalize = [&](int a) {
     double S = (kCarry && a) ? S1 : S0;
+    // lane L holds the trial's hits i = L - first (mod 32) (batches start at multiples of 32 in the
+    // stream); rotate into the canonical frame (lane c: hits i = c mod 32) before the fixed xor-tree
+    if constexpr (kCarry) S = __shfl_sync(FULL, S, (lane + (int)wt.first[a]) & 31);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) S += __shfl_xor_sync(FULL, S, off);
     if (lane == 0) p.ylt[wt.trial[a]] = clamp_terms(S, p.r3, p.l3);  // step 4: aggregate terms FT3
@@ -296,29 +299,23 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     for (int a = 0; a < 2; ++a)
       if (wt.state[a] == 2u && (int32_t)(done - wt.end[a]) >= 0) finalize(a);
   };
-  // Consume the pending batch: FT1/FT2 per row, rotate each trial's share into its canonical lanes.
+  // Consume the pending batch: FT1/FT2 per row, accumulated per trial.
   auto consume = [&]() {
     if (bn != 0) {
       if constexpr (kCarry) {
         const double o = rows.row_loss(p, s_r1, s_l1, pol_tab, rec_s, lane);
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          if (wt.state[a] == 0u) continue;  // warp-uniform
-          // this lane accumulates the trial's hit number (lane mod 32): batch slot src
-          const uint32_t src = ((uint32_t)lane + wt.first[a] - bstart) & 31u;
-          const double oa = __shfl_sync(FULL, o, (int)src);
-          const uint32_t rel = bstart + src - wt.first[a];  // position of that hit within trial a
-          // hits of trial a so far (all of them once scanned); batch positions are < issued
-          const uint32_t len_a = (wt.state[a] == 2u ? wt.end[a] : issued + ((qt - q_s) >> 2)) - wt.first[a];
-          if (src < (uint32_t)bn && rel < len_a) {
-            if (a) S1 += oa; else S0 += oa;
-          }
-          if (want_olt) {  // the maximum needs no canonical order: the source lane keeps it
-            const uint32_t relm = bstart + (uint32_t)lane - wt.first[a];
-            if (lane < bn && relm < len_a) {
-              if (a) M1 = o > M1 ? o : M1;
-              else M0 = o > M0 ? o : M0;
-            }
+        // Batch lane L holds stream position bstart + L (bstart is a multiple of 32).  It belongs to
+        // trial 0 if that trial is open and the position lies in its range, else to trial 1 (every
+        // queued hit belongs to one of the two open trials).  Each lane accumulates its own hits: no
+        // shuffles per batch (finalize rotates once per trial).
+        const uint32_t st0 = wt.state[0];
+        const uint32_t len0 = (st0 == 2u ? wt.end[0] : issued + ((qt - q_s) >> 2)) - wt.first[0];
+        const bool in0 = st0 != 0u && (bstart + (uint32_t)lane - wt.first[0]) < len0;
+        if (lane < bn) {
+          if (in0) S0 += o; else S1 += o;
+          if (want_olt) {  // the maximum needs no canonical order
+            if (in0) M0 = o > M0 ? o : M0;
+            else M1 = o > M1 ? o : M1;
           }
         }
       } else {
@@ -345,7 +342,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     __syncwarp();
     bstart = issued;
     bn = n;
-    issued += (uint32_t)n;
+    issued += 32u;  // a partial batch skips the rest of its 32 stream positions: batches stay 32-aligned
     qt -= 4u * (uint32_t)n;
     if constexpr (!kCarry) consume();  // wide rows: rows.issue already consumed round by round
   };
@@ -418,6 +415,24 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       e = b + p.K;
     }
     const uint32_t len = (uint32_t)(e - b);
+    // Bring this warp's NEXT trial into L2 with one bulk prefetch, so its windows (and the first one in
+    // particular) arrive at L2 latency: one window of register prefetch cannot cover DRAM latency.
+    if (lane == 0 && vec_ok) {
+      const uint64_t tn = t + (uint64_t)gridDim.x * NW;
+      if (tn < p.num_trials) {
+        uint64_t nb, ne;
+        if (p.offsets) {
+          nb = p.offsets[tn];
+          ne = p.offsets[tn + 1];
+        } else {
+          nb = tn * p.K;
+          ne = nb + p.K;
+        }
+        nb &= ~3ull;                                   // 16-B aligned start
+        ne = min((ne + 3u) & ~3ull, p.num_events & ~3ull);  // whole 16-B units inside the buffer
+        if (ne > nb && ne - nb <= (1u << 22)) prefetch_l2_bulk(p.ids + nb, (uint32_t)(ne - nb) * 4u);
+      }
+    }
     // Windows of 128 ids from the trial's first occurrence (so the order in which a trial's hits are
     // queued depends only on the trial itself): lane l holds window positions 4l .. 4l+3.  When the
     // trial start is 16-B aligned, full windows are single 16-B vectors streamed through a running
