@@ -166,6 +166,23 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(saddr), "l"(g), "l"(pol) : "memory");
 }
+// Streaming 16-byte load of 4 YET ids with no L2 policy operand (L1 no-allocate).
+__device__ __forceinline__ uint4 ld_ids4_stream(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_id_stream(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+// L2 prefetch of the 128-B line holding `g`.
+__device__ __forceinline__ void prefetch_l2_line(const void* g) {
+  asm volatile("prefetch.global.L2 [%0];" :: "l"(g));
+}
 // Bulk L2 prefetch of `bytes` (multiple of 16) from a 16-B aligned global address (one TMA request).
 __device__ __forceinline__ void prefetch_l2_bulk(const void* g, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(g), "r"(bytes) : "memory");

@@ -249,7 +249,6 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   __syncthreads();
 
   const uint64_t pol_tab = make_policy(true, p.l2_hints);
-  const uint64_t pol_yet = make_policy(false, p.l2_hints);
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(p.ids) & 15u) == 0);
   const uint32_t C = p.C;
   const uint32_t fmul = p.fold_mul;
@@ -415,22 +414,15 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       e = b + p.K;
     }
     const uint32_t len = (uint32_t)(e - b);
-    // Bring this warp's NEXT trial into L2 with one bulk prefetch, so its windows (and the first one in
-    // particular) arrive at L2 latency: one window of register prefetch cannot cover DRAM latency.
-    if (lane == 0 && vec_ok) {
+    // Bring this warp's NEXT trial into L2 (lane l prefetches its 128-B line l: the first 4 KB), so its
+    // windows arrive at L2 latency: one window of register prefetch cannot cover DRAM latency.
+    {
       const uint64_t tn = t + (uint64_t)gridDim.x * NW;
       if (tn < p.num_trials) {
-        uint64_t nb, ne;
-        if (p.offsets) {
-          nb = p.offsets[tn];
-          ne = p.offsets[tn + 1];
-        } else {
-          nb = tn * p.K;
-          ne = nb + p.K;
-        }
-        nb &= ~3ull;                                   // 16-B aligned start
-        ne = min((ne + 3u) & ~3ull, p.num_events & ~3ull);  // whole 16-B units inside the buffer
-        if (ne > nb && ne - nb <= (1u << 22)) prefetch_l2_bulk(p.ids + nb, (uint32_t)(ne - nb) * 4u);
+        const uint64_t nb = p.offsets ? p.offsets[tn] : tn * p.K;
+        const uint64_t ne = p.offsets ? p.offsets[tn + 1] : nb + p.K;
+        const uint64_t g = nb + 32u * (uint32_t)lane;  // id index of this lane's line
+        if (g < ne && g < p.num_events) prefetch_l2_line(p.ids + g);
       }
     }
     // Windows of 128 ids from the trial's first occurrence (so the order in which a trial's hits are
@@ -444,25 +436,29 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     auto load_checked = [&](uint32_t w) -> uint4 {
       const uint32_t r = w * 128u + 4u * lane;  // trial position of this lane's first slot
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (vec && r + 4u <= len) return ld_ids4(p.ids + b + r, pol_yet);
-      if (r < len) v.x = ld_id(p.ids + b + r, pol_yet);
-      if (r + 1u < len) v.y = ld_id(p.ids + b + r + 1, pol_yet);
-      if (r + 2u < len) v.z = ld_id(p.ids + b + r + 2, pol_yet);
-      if (r + 3u < len) v.w = ld_id(p.ids + b + r + 3, pol_yet);
+      if (vec && r + 4u <= len) return ld_ids4_stream(p.ids + b + r);
+      if (r < len) v.x = ld_id_stream(p.ids + b + r);
+      if (r + 1u < len) v.y = ld_id_stream(p.ids + b + r + 1);
+      if (r + 2u < len) v.z = ld_id_stream(p.ids + b + r + 2);
+      if (r + 3u < len) v.w = ld_id_stream(p.ids + b + r + 3);
       return v;
     };
     auto rel0 = [&](uint32_t w) -> uint32_t { return w * 128u + 4u * (uint32_t)lane; };
     uint32_t w = 0;
-    if (wf1 != 0u) {  // full windows: running pointer, one window held ahead
+    if (wf1 != 0u) {  // full windows: running pointer, one window held ahead (two register sets, unrolled)
       const uint4* lp = reinterpret_cast<const uint4*>(p.ids + b) + lane;
-      uint4 cur = ld_ids4(reinterpret_cast<const uint32_t*>(lp), pol_yet);
-      for (uint32_t rem = wf1 - 1u;; --rem) {
-        lp += 32;
-        uint4 nxt;  // only read when rem != 0, i.e. when loaded
-        if (rem != 0u) nxt = ld_ids4(reinterpret_cast<const uint32_t*>(lp), pol_yet);
-        scan(cur, BoolC<false>{}, 0u, 0u);
+      uint4 wa = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp)), wb;
+      uint32_t rem = wf1 - 1u;  // full windows after the one in wa
+      while (true) {
+        if (rem != 0u) wb = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp + 32));
+        scan(wa, BoolC<false>{}, 0u, 0u);
         if (rem == 0u) break;
-        cur = nxt;
+        --rem;
+        lp += 64;
+        if (rem != 0u) wa = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp));
+        scan(wb, BoolC<false>{}, 0u, 0u);
+        if (rem == 0u) break;
+        --rem;
       }
       w = wf1;
     }
