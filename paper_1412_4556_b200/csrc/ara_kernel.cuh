@@ -194,6 +194,38 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t saddr) {
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr) : "memory");
   return v;
 }
+// Presence-queue insertion for a pair of window slots (presence kernel).  wa/wb: the bitmap words of
+// the two ids, xa/xb: their bit indices (mod 32); the lane's first hit of the pair is appended at
+// qt + 4 * (hits of lower lanes), then -- only if some lane hit both -- the second ids likewise; qt
+// (the queue's shared tail address) advances by 4 per appended id.  One ballot per pair; the hit
+// tests stay predicates end to end (written in PTX so no 0/1 integers are materialised).
+__device__ __forceinline__ void pair_insert(uint32_t wa, uint32_t xa, uint32_t ida, uint32_t wb, uint32_t xb,
+                                            uint32_t idb, uint32_t lt, uint32_t& qt) {
+  asm volatile(
+      "{\n"
+      " .reg .pred pa, pb, pany, pboth, pq;\n"
+      " .reg .b32 sa, sb, ma, mb, f, m, t, a, c;\n"
+      " and.b32 sa, %2, 31;\n shl.b32 ma, 1, sa;\n and.b32 ma, ma, %1;\n setp.ne.b32 pa, ma, 0;\n"
+      " and.b32 sb, %5, 31;\n shl.b32 mb, 1, sb;\n and.b32 mb, mb, %4;\n setp.ne.b32 pb, mb, 0;\n"
+      " or.pred pany, pa, pb;\n and.pred pboth, pa, pb;\n"
+      " selp.b32 f, %3, %6, pa;\n"
+      " vote.sync.ballot.b32 m, pany, 0xffffffff;\n"
+      " and.b32 t, m, %7;\n popc.b32 t, t;\n mad.lo.u32 a, t, 4, %0;\n"
+      " @pany st.shared.u32 [a], f;\n"
+      " popc.b32 c, m;\n mad.lo.u32 %0, c, 4, %0;\n"
+      " vote.sync.any.pred pq, pboth, 0xffffffff;\n"
+      " @!pq bra.uni PAIR_DONE_%=;\n"
+      " vote.sync.ballot.b32 m, pboth, 0xffffffff;\n"
+      " and.b32 t, m, %7;\n popc.b32 t, t;\n mad.lo.u32 a, t, 4, %0;\n"
+      " @pboth st.shared.u32 [a], %6;\n"
+      " popc.b32 c, m;\n mad.lo.u32 %0, c, 4, %0;\n"
+      "PAIR_DONE_%=:\n"
+      "}\n"
+      : "+r"(qt)
+      : "r"(wa), "r"(xa), "r"(ida), "r"(wb), "r"(xb), "r"(idb), "r"(lt)
+      : "memory");
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

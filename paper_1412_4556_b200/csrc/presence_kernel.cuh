@@ -352,39 +352,22 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     }
     consume();
   };
-  // Presence test of one id (see above): one VIADDMNMX, IMAD.HI, LDS, shift, and.
-  auto present = [&](uint32_t id) -> bool {
-    const uint32_t x = min(id - 1u, C);
-    return (bits[__umulhi(x, fmul)] >> (x & 31u)) & 1u;
-  };
   // Scan one window: lane l holds window positions 4l .. 4l+3 (ids v); CHECKED windows mask positions
   // outside the trial (r = window position of id 0 relative to the trial start, len = trial length).
   auto scan = [&](const uint4 v, auto checked, uint32_t r, uint32_t len) {
     const uint32_t id[4] = {v.x, v.y, v.z, v.w};
-    bool hit[4];
+    uint32_t x[4], wd[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      hit[u] = present(id[u]);
-      if constexpr (decltype(checked)::value) hit[u] = hit[u] && (r + (uint32_t)u < len);
+      x[u] = min(id[u] - 1u, C);          // invalid ids -> the sentinel bit C
+      wd[u] = bits[__umulhi(x[u], fmul)];  // the folded bitmap word holding bit x & 31
+      if constexpr (decltype(checked)::value) wd[u] = (r + (uint32_t)u < len) ? wd[u] : 0u;  // outside the trial
     }
     // Append the hits in a fixed order that depends only on the window: per pair of slots, first the
     // lanes' first hit of the pair (lanes ascending), then -- only if some lane hit both -- the
     // second ids of those lanes.  One ballot per pair instead of one per slot.
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool ha = hit[2 * h], hb = hit[2 * h + 1];
-      const bool any = ha || hb;
-      const uint32_t first = ha ? id[2 * h] : id[2 * h + 1];
-      const unsigned m = ballot_full(any);
-      sts_u32_if(qt + 4u * __popc(m & lt), first, any);
-      qt += 4u * __popc(m);
-      const bool both = ha && hb;
-      if (any_full(both)) {  // rare: ~1% of lanes per pair
-        const unsigned m2 = ballot_full(both);
-        sts_u32_if(qt + 4u * __popc(m2 & lt), id[2 * h + 1], both);
-        qt += 4u * __popc(m2);
-      }
-    }
+    pair_insert(wd[0], x[0], id[0], wd[1], x[1], id[1], lt, qt);
+    pair_insert(wd[2], x[2], id[2], wd[3], x[3], id[3], lt, qt);
     // warp-uniform; at most 31 + 128 = 159 < kQueue queued
     while (qt - q_s >= 128u) issue(32);
   };
