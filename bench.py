@@ -557,13 +557,18 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
     from paper_1412_4556_b200 import ara
     nv = info[0]["num_variants"]
     rb = max(32, info[0]["row_stride"])
+    presence = info[0]["variant"].startswith("ara_presence")
     for v in range(nv):
-        for bt in (128, 256):
-            for bps in (0,) if info[0]["variant"].startswith("ara_presence") else (0, 2, 3, 4, 6, 8):
+        # presence kernels fix their block size: sweep the next-trial prefetch instead of block threads
+        for bt in ((0, 1) if presence else (128, 256)):
+            for bps in (0,) if presence else (0, 2, 3, 4, 6, 8):
                 for pol in (0, 1, 2):
                     try:
                         ctx.ara_set_option(ara.ARA_OPT_VARIANT, v)
-                        ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, bt)
+                        if presence:
+                            ctx.ara_set_option(ara.ARA_OPT_PREFETCH, bt)
+                        else:
+                            ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, bt)
                         ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, bps)
                         ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, pol)
                     except ara.AraError:
@@ -577,9 +582,12 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
                     b.record(stream)
                     torch.cuda.synchronize()
                     ms = a.elapsed_time(b) / 5 / L
-                    print(json.dumps({"sweep": ctx.ara_layer_info(0)["variant"], "block": bt, "bps": bps, "l2_policy": pol,
+                    print(json.dumps({"sweep": ctx.ara_layer_info(0)["variant"], ("prefetch" if presence else "block"): bt,
+                                      "bps": bps, "l2_policy": pol,
                                       "launch_ms": ms, "eff_GBps": occ * (4 + rb) / ms / 1e6}), file=sys.stderr, flush=True)
     ctx.ara_set_option(ara.ARA_OPT_VARIANT, 0)
+    if presence:
+        ctx.ara_set_option(ara.ARA_OPT_PREFETCH, 1)
     ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, 0)
     ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, 0)
     ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, 0)

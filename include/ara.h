@@ -196,8 +196,11 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
 /* Tuning knobs (launch-shape sweep; L2 policy).  0 = library default.
  *   ARA_OPT_BLOCK_THREADS   threads per block (multiple of 32, <= 1024)
  *   ARA_OPT_BLOCKS_PER_SM   resident blocks per SM the persistent grid is sized for
- *   ARA_OPT_L2_POLICY       0 default (evict_last hints on table rows, evict_first on YET ids),
- *                           1 no hints, 2 hints + persisting access-policy window on the table
+ *   ARA_OPT_L2_POLICY       0 default (evict_last hints on table rows and records; the dense kernel
+ *                           also marks YET ids evict_first), 1 no hints, 2 hints + persisting
+ *                           access-policy window on the table
+ *   ARA_OPT_PREFETCH        presence kernel: 1 (default) each warp prefetches its next trial's ids
+ *                           into L2 at the start of a trial, 0 off
  *   ARA_OPT_VARIANT         kernel variant index within the selected kernel and row width
  *                           (ara_layer_info reports the count)
  *   ARA_OPT_KERNEL          -1 auto (default): per layer, the presence kernel when its folded bitmap is
@@ -214,7 +217,8 @@ typedef enum {
   ARA_OPT_BLOCKS_PER_SM = 2,
   ARA_OPT_L2_POLICY = 3,
   ARA_OPT_VARIANT = 4,
-  ARA_OPT_KERNEL = 5
+  ARA_OPT_KERNEL = 5,
+  ARA_OPT_PREFETCH = 6
 } ara_option;
 ARA_API ara_status ara_set_option(ara_ctx* ctx, ara_option opt, int64_t value);
 ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);

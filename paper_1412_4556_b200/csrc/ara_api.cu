@@ -95,6 +95,7 @@ struct ara_ctx {
   int block_threads = 256;
   int blocks_per_sm = 0;
   int l2_policy = 0;
+  int prefetch = 1;
   int variant = 0;
   int kernel = -1;  // KernelKind, or -1 = per-layer automatic choice
   int persist_max = 0, window_max = 0;
@@ -281,6 +282,7 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   p.C = c->C;
   p.jpad = L.jpad;
   p.l2_hints = c->l2_policy == 1 ? 0u : 1u;
+  p.prefetch = c->prefetch ? 1u : 0u;
   p.ylt = ylt;
   p.olt = olt;
   p.err = c->d_err;
@@ -794,6 +796,10 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
       c->kernel = (int)v;
       c->variant = 0;
       return ARA_OK;
+    case ARA_OPT_PREFETCH:
+      if (v < 0 || v > 1) return set_error(ARA_E_ARG, "prefetch in {0, 1}");
+      c->prefetch = (int)v;
+      return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }
@@ -806,6 +812,7 @@ ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
     case ARA_OPT_L2_POLICY: *v = c->l2_policy; return ARA_OK;
     case ARA_OPT_VARIANT: *v = c->variant; return ARA_OK;
     case ARA_OPT_KERNEL: *v = c->kernel; return ARA_OK;
+    case ARA_OPT_PREFETCH: *v = c->prefetch; return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }

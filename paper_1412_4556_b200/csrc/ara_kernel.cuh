@@ -38,6 +38,7 @@ struct LayerParams {
   uint32_t C;                // catalogue size
   uint32_t jpad;             // row stride in floats
   uint32_t l2_hints;         // 1: evict_last / evict_first policies; 0: evict_normal
+  uint32_t prefetch;         // presence kernel: 1 = L2 prefetch of the warp's next trial
   double* ylt;               // this layer's YLT row (num_trials doubles)
   double* olt;               // this layer's OLT row (largest occurrence-net loss per trial) or nullptr
   unsigned* err;             // bit0: id out of range, bit1: bad offsets

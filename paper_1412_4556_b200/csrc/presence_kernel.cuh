@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     const uint32_t len = (uint32_t)(e - b);
     // Bring this warp's NEXT trial into L2 (lane l prefetches its 128-B line l: the first 4 KB), so its
     // windows arrive at L2 latency: one window of register prefetch cannot cover DRAM latency.
-    {
+    if (p.prefetch) {
       const uint64_t tn = t + (uint64_t)gridDim.x * NW;
       if (tn < p.num_trials) {
         const uint64_t nb = p.offsets ? p.offsets[tn] : tn * p.K;
