@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(kSelBlock) tail_pass(const double* __restrict_
 // barriers.  Each block keeps its contiguous chunk of keys in shared memory (when it fits), so the
 // YLT is read from HBM once; every block redundantly derives the per-query digits from the final
 // global histogram of the pass (triple-buffered so it can be cleared two passes ahead).
-constexpr int kFusedBlock = 256;
-constexpr int kCacheKeys = 4096;  // 32 KB of cached keys per block
+constexpr int kFusedBlock = 1024;   // one block per SM: fewer arrivals at each grid barrier
+constexpr int kCacheKeys = 8192;    // 64 KB of cached keys per block (N <= 1.2M on 148 SMs)
 
 struct FusedState {  // zeroed (cudaMemsetAsync) before every launch
   unsigned int H[3][kMaxQ][256];
@@ -301,12 +301,15 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
       const uint64_t key = valid ? (cached ? skeys[i] : to_key(y[lo + i])) : 0;
       const unsigned digit = (unsigned)(key >> shift) & 0xffu;
       const uint64_t hik = pass == 0 ? 0 : (key >> (shift + 8));
-      for (int sl = 0; sl < ns; ++sl) {
-        const bool hit = valid && hik == s_slot_prefix[sl];
-        if (!__any_sync(FULL, hit)) continue;
-        const unsigned peers = __match_any_sync(FULL, hit ? digit : 0x100u);
-        if (hit && (__ffs(peers) - 1) == lane) atomicAdd(&sh[sl][digit], __popc(peers));
-      }
+      // the slots' prefixes are distinct, so a key feeds at most one slot's histogram
+      int sl = -1;
+      if (valid)
+        for (int j = 0; j < ns; ++j)
+          if (hik == s_slot_prefix[j]) sl = j;
+      if (!__any_sync(FULL, sl >= 0)) continue;
+      const unsigned bin = sl >= 0 ? ((unsigned)sl << 8 | digit) : 0xffffffffu;
+      const unsigned peers = __match_any_sync(FULL, bin);  // warp-aggregated shared atomics
+      if (sl >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&sh[sl][digit], __popc(peers));
     }
     __syncthreads();
     unsigned int(*H)[256] = st->H[pass % 3];
@@ -319,55 +322,82 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
     grid_sync(&st->bar_count, &st->bar_gen, nb);
     for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) sh[i / 256][i % 256] = ((volatile unsigned int*)H[i / 256])[i % 256];
     __syncthreads();
-    if (threadIdx.x < m) {
-      const int q = threadIdx.x;
+    if (w < m) {  // warp q: the digit d of query q's k-th largest key among the keys of its slot
+      const int q = w;
       const unsigned int* h = sh[s_q2slot[q]];
-      uint64_t r = s_rank[q], above = 0;
-      int d = 255;
-      for (; d > 0; --d) {
-        const uint64_t c = h[d];
-        if (above + c >= r) break;
-        above += c;
+      const uint64_t r = s_rank[q];
+      // lane l owns digits 255 - 8l .. 248 - 8l (descending); exclusive prefix of the lane totals
+      uint64_t c[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = h[255 - 8 * lane - j];
+        tot += c[j];
       }
-      s_rank[q] = r - above;
-      s_prefix[q] = (s_prefix[q] << 8) | (uint64_t)d;
+      uint64_t above = tot;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(FULL, above, off);
+        if (lane >= off) above += o;
+      }
+      above -= tot;  // count of keys in the slot with a larger digit than this lane's bins
+      // the lane whose range holds rank r finds its digit (digit 0 if the rank runs past every bin)
+      const bool mine = above < r && (r <= above + tot || lane == 31);
+      const unsigned who = __ballot_sync(FULL, mine);
+      const int src = __ffs(who) - 1;
+      int d = 0;
+      uint64_t ab = above;
+      if (lane == src) {
+        d = 248 - 8 * lane;  // lowest digit of the range (taken if the rank runs past it)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int dj = 255 - 8 * lane - j;
+          if (ab + c[j] >= r) {
+            d = dj;
+            break;
+          }
+          if (dj == 0) {  // rank beyond the slot's keys cannot happen for a valid k; keep digit 0
+            d = 0;
+            break;
+          }
+          ab += c[j];
+        }
+      }
+      d = __shfl_sync(FULL, d, src);
+      ab = __shfl_sync(FULL, ab, src);
+      if (lane == 0) {
+        s_rank[q] = r - ab;
+        s_prefix[q] = (s_prefix[q] << 8) | (uint64_t)d;
+      }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int k = 0;
-      for (int q = 0; q < m; ++q) {
-        int sl = 0;
-        while (sl < k && s_slot_prefix[sl] != s_prefix[q]) ++sl;
-        if (sl == k) s_slot_prefix[k++] = s_prefix[q];
-        s_q2slot[q] = sl;
+    if (w == 0) {  // slots = distinct prefixes, numbered in query order
+      const uint64_t pq = lane < m ? s_prefix[lane] : ~0ull;
+      int first = lane;
+      for (int q2 = 0; q2 < m; ++q2)
+        if (q2 < first && s_prefix[q2] == pq) first = q2;
+      const unsigned leaders = __ballot_sync(FULL, lane < m && first == lane);
+      if (lane < m) {
+        const int sl = __popc(leaders & ((1u << first) - 1u));
+        s_q2slot[lane] = sl;
+        if (first == lane) s_slot_prefix[sl] = pq;
       }
-      s_nslot = k;
+      if (lane == 0) s_nslot = __popc(leaders);
     }
     __syncthreads();
   }
-  // tail: count and fp64-sum the values above each query's threshold T (fixed reduction order)
-  double sacc[kMaxQ];
-  unsigned long long cacc[kMaxQ];
-#pragma unroll
-  for (int q = 0; q < kMaxQ; ++q) {
-    sacc[q] = 0.0;
-    cacc[q] = 0;
-  }
-  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const uint64_t key = cached ? skeys[i] : to_key(y[lo + i]);
-    const double v = from_key(key);
-#pragma unroll
-    for (int q = 0; q < kMaxQ; ++q)
-      if (q < m && key > s_prefix[q]) {
-        sacc[q] += v;
-        cacc[q] += 1;
+  // tail: count and fp64-sum the values above each query's threshold T (fixed reduction order), one
+  // query at a time so each thread holds a single accumulator pair
+  for (int q = 0; q < m; ++q) {
+    const uint64_t pq = s_prefix[q];
+    double a = 0.0;
+    unsigned long long b = 0;
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const uint64_t key = cached ? skeys[i] : to_key(y[lo + i]);
+      if (key > pq) {
+        a += from_key(key);
+        b += 1;
       }
-  }
-#pragma unroll
-  for (int q = 0; q < kMaxQ; ++q) {
-    if (q >= m) break;
-    double a = sacc[q];
-    unsigned long long b = cacc[q];
+    }
     for (int off = 16; off > 0; off >>= 1) {
       a += __shfl_xor_sync(FULL, a, off);
       b += __shfl_xor_sync(FULL, b, off);
@@ -390,10 +420,11 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
   }
   grid_sync(&st->bar_count, &st->bar_gen, nb);
   if (blockIdx.x != 0) return;
-  for (int q = 0; q < m; ++q) {
+  if (w < m) {  // warp q combines the block partials of query q in a fixed order
+    const int q = w;
     double a = 0.0;
     unsigned long long b = 0;
-    for (unsigned i = threadIdx.x; i < nb; i += blockDim.x) {
+    for (unsigned i = lane; i < nb; i += 32) {
       a += ((volatile double*)psum)[(uint64_t)i * kMaxQ + q];
       b += ((volatile unsigned long long*)pcnt)[(uint64_t)i * kMaxQ + q];
     }
@@ -402,23 +433,11 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
       b += __shfl_xor_sync(FULL, b, off);
     }
     if (lane == 0) {
-      wsum[w][q] = a;
-      wcnt[w][q] = b;
+      const double T = from_key(s_prefix[q]);
+      const uint64_t k = Q.k[q];
+      if (pml_out) pml_out[q] = T;  // PML: the k-th largest value
+      if (tvar_out) tvar_out[q] = __ddiv_rn(__dadd_rn(a, __dmul_rn((double)(k - b), T)), (double)k);  // TVaR
     }
-  }
-  __syncthreads();
-  if (threadIdx.x < m) {
-    const int q = threadIdx.x;
-    double a = 0.0;
-    unsigned long long b = 0;
-    for (int i = 0; i < kFusedBlock / 32; ++i) {
-      a += wsum[i][q];
-      b += wcnt[i][q];
-    }
-    const double T = from_key(s_prefix[q]);
-    const uint64_t k = Q.k[q];
-    if (pml_out) pml_out[q] = T;  // PML: the k-th largest value
-    if (tvar_out) tvar_out[q] = __ddiv_rn(__dadd_rn(a, __dmul_rn((double)(k - b), T)), (double)k);  // TVaR
   }
 }
 
