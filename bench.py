@@ -452,7 +452,7 @@ def main():
     if os.path.exists(prof):
         with open(prof) as f:
             pj = json.load(f)
-        if pj.get("variant") == info[0]["variant"]:
+        if pj.get("variant") == info[0]["variant"] and world == 1:  # the capture is of the N = 1 launch
             traffic = pj.get("dram_bytes_per_launch")
 
     # ---- the dense direct-access kernel (every occurrence gathers its full row), timed beside
@@ -489,7 +489,9 @@ def main():
         "config": {"workload": f"{cfg.name}: {cfg.description}", "num_trials": N,
                    "events_per_trial": [cfg.kmin, cfg.kmax], "layers": L, "elts_per_layer": len(cfg.layers[0].elts),
                    "catalog": cfg.catalog_size, "entries_per_elt": cfg.entries_per_elt, "regime": cfg.regime,
-                   "parallelism": f"trial-sharded x{world}" + (" + NCCL YLT all-gather" if world > 1 else ""),
+                   "parallelism": f"trial-sharded x{world}" + (
+                       (" + NCCL YLT all-gather" if args.dist_backend == "nccl" else " + gloo YLT all-gather (host)")
+                       if world > 1 else ""),
                    "l2": "no flush: inputs (YET %.1f GB) exceed L2; table L2-resident by design (cold_l2_ms beside)"
                          % (n_ids * 4 / 1e9),
                    "kernel": info[0]["variant"], "storage": "fp32 ELT losses, fp64 terms/sums/YLT"},
