@@ -204,8 +204,10 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *   ARA_OPT_VARIANT         kernel variant index within the selected kernel and row width
  *                           (ara_layer_info reports the count)
  *   ARA_OPT_KERNEL          -1 auto (default): per layer, the presence kernel when its folded bitmap is
- *                           expected to send at most 25% of the occurrences (15% for J > 16) to the
- *                           row gather, else the dense kernel;
+ *                           expected to send at most 60% of the occurrences to the gather (25% when
+ *                           more than 5% of the non-zero rows hold more than two losses: those rows
+ *                           are read in full instead of through their 16-B sparse record), else the
+ *                           dense kernel;
  *                           0 presence: a per-layer presence bitmap of the table's non-zero rows,
  *                           staged in shared memory, so only rows that hold a loss are gathered;
  *                           1 dense: every occurrence gathers its full row.  Identical results (an

@@ -67,7 +67,7 @@ struct Layer {
   uint32_t* folded = nullptr;   // the bitmap folded for the presence kernel's shared memory (same size)
   uint32_t folded_words = 0;    // words of the current fold (0: not built yet)
   uint32_t fold_mul = 0;        // its multiplier (LayerParams::fold_mul)
-  uint4* rec = nullptr;         // sparse row records (C + 1) x 16 B, rows of <= 16 columns
+  uint4* rec = nullptr;         // sparse row records (C + 1) x 16 B (presence kernels with one lane per row)
   // Section IV.B study structures, built on first use by ara_run_study
   float* indep = nullptr;         // J x (C + 1) independent per-ELT direct-access arrays
   uint32_t* sorted_ids = nullptr; // per-ELT (event, loss) pairs sorted by event
@@ -251,9 +251,9 @@ static void destroy_ctx(ara_ctx* c) {
 }
 
 // Dynamic shared memory of a presence variant besides the bitmap: the per-warp hit queues and, for
-// narrow rows (record batches), 32 x 16-B record slots per warp (+16 B alignment slack).
+// one-lane-per-row variants (record batches), 32 x 16-B record slots per warp (+16 B alignment slack).
 static size_t presence_warp_smem(const Variant* v) {
-  const bool rec = v->G == 1 && v->V * v->NV <= 16;
+  const bool rec = v->G == 1;
   return (size_t)v->NW * kQueue * 4 + (rec ? (size_t)v->NW * 512 + 16 : 0);
 }
 
@@ -483,12 +483,19 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
     }
     CK(cudaMemsetAsync(L.present, 0, (size_t)L.present_words * 4, s));
     {  // presence statistics -> automatic kernel choice (see ara.h, ARA_OPT_KERNEL)
-      std::vector<uint64_t> row((catalog_size + 64ull) / 64, 0);
+      std::vector<uint8_t> cnt((uint64_t)catalog_size + 1, 0);  // non-zero losses per row, saturating at 3
       for (uint32_t m = 0; m < L.J; ++m) {
         const ara_elt& e = elts[in.elt_index[m]];
-        for (uint64_t i = 0; i < e.num_entries; ++i) row[e.event_ids[i] >> 6] |= 1ull << (e.event_ids[i] & 63);
+        for (uint64_t i = 0; i < e.num_entries; ++i) {
+          uint8_t& k = cnt[e.event_ids[i]];
+          k = k < 3 ? (uint8_t)(k + 1) : k;
+        }
       }
-      for (uint64_t w : row) L.present_rows += (uint64_t)__builtin_popcountll(w);
+      uint64_t multi = 0;  // rows with more than two losses: read in full by the record path
+      for (uint8_t k : cnt) {
+        L.present_rows += k != 0;
+        multi += k > 2;
+      }
       const Variant* pv = L.variants[KIND_PRESENCE][0];
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, (const void*)pv->fn));
@@ -497,9 +504,12 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       const double fw = budget > 0 ? std::min(pw, (double)(budget / 4)) : 1.0;
       const double dens = (double)L.present_rows / ((double)catalog_size + 1.0);
       L.est_hit_rate = 1.0 - pow(1.0 - dens, std::max(1.0, pw / fw));
-      // the presence kernel pays off while it skips most rows; wide rows (J > 16) gather 13+ sectors
-      // per hit in round-by-round batches, so they need a sparser bitmap
-      L.auto_kind = (budget >= 4096 && L.est_hit_rate <= (L.jpad <= 16 ? 0.25 : 0.15)) ? KIND_PRESENCE : KIND_DENSE;
+      // The presence kernel pays off while it skips most rows.  With one lane per row (G = 1) a hit
+      // fetches its 16-B sparse record, not the row, unless the row holds more than two losses; with
+      // full-row batches (G > 1) wide rows gather 13+ sectors per hit in rounds and need a sparser bitmap.
+      const double multi_share = L.present_rows ? (double)multi / (double)L.present_rows : 0.0;
+      const double lim = pv->G == 1 ? (multi_share <= 0.05 ? 0.6 : 0.25) : (L.jpad <= 16 ? 0.25 : 0.15);
+      L.auto_kind = (budget >= 4096 && L.est_hit_rate <= lim) ? KIND_PRESENCE : KIND_DENSE;
     }
     h_ids.clear();
     h_col.clear();
@@ -523,16 +533,6 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       CK(cudaGetLastError());
       presence_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(L.present, d_ids, n);
       CK(cudaGetLastError());
-      if (L.jpad <= 16) {  // sparse records for the narrow-row presence kernel
-        if (cudaMalloc(&L.rec, ((uint64_t)catalog_size + 1) * sizeof(uint4)) != cudaSuccess) {
-          cudaGetLastError();
-          FAIL(set_error(ARA_E_NOMEM, "row records for layer %u", l));
-        }
-        const uint64_t rows = (uint64_t)catalog_size + 1;
-        const uint64_t rb = std::min<uint64_t>((rows + 255) / 256, (uint64_t)c->sms * 16);
-        record_build_kernel<<<(unsigned)rb, 256, 0, s>>>(L.rec, L.table, L.jpad, rows);
-        CK(cudaGetLastError());
-      }
       CK(cudaStreamSynchronize(s));  // host staging vectors are reused for the next layer
       cudaFree(d_ids);
       cudaFree(d_col);
@@ -540,6 +540,16 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       d_ids = nullptr;
       d_col = nullptr;
       d_loss = nullptr;
+    }
+    {  // sparse row records for the one-lane-per-row presence kernels (every row width <= kMaxJ)
+      if (cudaMalloc(&L.rec, ((uint64_t)catalog_size + 1) * sizeof(uint4)) != cudaSuccess) {
+        cudaGetLastError();
+        FAIL(set_error(ARA_E_NOMEM, "row records for layer %u", l));
+      }
+      const uint64_t rows = (uint64_t)catalog_size + 1;
+      const uint64_t rb = std::min<uint64_t>((rows + 255) / 256, (uint64_t)c->sms * 16);
+      record_build_kernel<<<(unsigned)rb, 256, 0, s>>>(L.rec, L.table, L.jpad, rows);
+      CK(cudaGetLastError());
     }
   }
   CK(cudaStreamSynchronize(s));

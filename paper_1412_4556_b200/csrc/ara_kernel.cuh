@@ -200,14 +200,15 @@ __device__ __forceinline__ uint4 lds_u128(uint32_t saddr) {
 // qt + 4 * (hits of lower lanes), then -- only if some lane hit both -- the second ids likewise; qt
 // (the queue's shared tail address) advances by 4 per appended id.  One ballot per pair; the hit
 // tests stay predicates end to end (written in PTX so no 0/1 integers are materialised).
+// `valid` masks the two slots (all ones for full windows; ptxas folds the AND into the test's LOP3).
 __device__ __forceinline__ void pair_insert(uint32_t wa, uint32_t xa, uint32_t ida, uint32_t wb, uint32_t xb,
-                                            uint32_t idb, uint32_t lt, uint32_t& qt) {
+                                            uint32_t idb, uint32_t lt, uint32_t& qt, uint32_t valid = 0xffffffffu) {
   asm volatile(
       "{\n"
       " .reg .pred pa, pb, pany, pboth, pq;\n"
       " .reg .b32 sa, sb, ma, mb, f, m, t, a, c;\n"
-      " and.b32 sa, %2, 31;\n shl.b32 ma, 1, sa;\n and.b32 ma, ma, %1;\n setp.ne.b32 pa, ma, 0;\n"
-      " and.b32 sb, %5, 31;\n shl.b32 mb, 1, sb;\n and.b32 mb, mb, %4;\n setp.ne.b32 pb, mb, 0;\n"
+      " and.b32 sa, %2, 31;\n shl.b32 ma, 1, sa;\n and.b32 ma, ma, %1;\n and.b32 ma, ma, %8;\n setp.ne.b32 pa, ma, 0;\n"
+      " and.b32 sb, %5, 31;\n shl.b32 mb, 1, sb;\n and.b32 mb, mb, %4;\n and.b32 mb, mb, %8;\n setp.ne.b32 pb, mb, 0;\n"
       " or.pred pany, pa, pb;\n and.pred pboth, pa, pb;\n"
       " selp.b32 f, %3, %6, pa;\n"
       " vote.sync.ballot.b32 m, pany, 0xffffffff;\n"
@@ -223,8 +224,21 @@ __device__ __forceinline__ void pair_insert(uint32_t wa, uint32_t xa, uint32_t i
       "PAIR_DONE_%=:\n"
       "}\n"
       : "+r"(qt)
-      : "r"(wa), "r"(xa), "r"(ida), "r"(wb), "r"(xb), "r"(idb), "r"(lt)
+      : "r"(wa), "r"(xa), "r"(ida), "r"(wb), "r"(xb), "r"(idb), "r"(lt), "r"(valid)
       : "memory");
+}
+
+// Read-only shared loads (no volatile, no memory clobber: the bitmap and the FT1 terms are written once
+// before the kernel's __syncthreads, so these may be scheduled and hoisted freely).
+__device__ __forceinline__ uint32_t lds_ro_u32(uint32_t saddr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+__device__ __forceinline__ double2 lds_ro_f64x2(uint32_t saddr) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(saddr));
+  return v;
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

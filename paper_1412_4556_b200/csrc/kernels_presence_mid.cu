@@ -10,14 +10,14 @@ namespace ara {
 
 
 static const Variant kTable[] = {
-    // first per row width = default (B200 sweeps)
-    ARA_PRES(8, 3, 2, 16), ARA_PRES(8, 3, 4, 16), ARA_PRES(8, 3, 2, 24),
-    ARA_PRES(8, 4, 2, 16), ARA_PRES(8, 4, 4, 16), ARA_PRES(8, 4, 2, 24),
-    ARA_PRES(8, 5, 16, 16), ARA_PRES(8, 5, 8, 16), ARA_PRES(8, 5, 16, 24),
-    ARA_PRES(8, 6, 16, 16), ARA_PRES(8, 6, 8, 16), ARA_PRES(8, 6, 16, 24),
-    ARA_PRES(8, 7, 16, 16), ARA_PRES(8, 7, 8, 16), ARA_PRES(8, 7, 16, 24),
-    ARA_PRES(8, 8, 16, 16), ARA_PRES(8, 8, 8, 16), ARA_PRES(8, 8, 16, 24),
-    ARA_PRES(8, 9, 16, 16), ARA_PRES(8, 9, 8, 16), ARA_PRES(8, 9, 16, 24),
+    // first per row width = default: one lane per row with sparse records (G = 1); then full-row batches
+    ARA_PRES(8, 3, 1, 32), ARA_PRES(8, 3, 2, 16), ARA_PRES(8, 3, 4, 16), ARA_PRES(8, 3, 2, 24),
+    ARA_PRES(8, 4, 1, 32), ARA_PRES(8, 4, 2, 16), ARA_PRES(8, 4, 4, 16), ARA_PRES(8, 4, 2, 24),
+    ARA_PRES(8, 5, 1, 32), ARA_PRES(8, 5, 16, 16), ARA_PRES(8, 5, 8, 16), ARA_PRES(8, 5, 16, 24),
+    ARA_PRES(8, 6, 1, 32), ARA_PRES(8, 6, 16, 16), ARA_PRES(8, 6, 8, 16), ARA_PRES(8, 6, 16, 24),
+    ARA_PRES(8, 7, 1, 32), ARA_PRES(8, 7, 16, 16), ARA_PRES(8, 7, 8, 16), ARA_PRES(8, 7, 16, 24),
+    ARA_PRES(8, 8, 1, 32), ARA_PRES(8, 8, 16, 16), ARA_PRES(8, 8, 8, 16), ARA_PRES(8, 8, 16, 24),
+    ARA_PRES(8, 9, 1, 32), ARA_PRES(8, 9, 16, 16), ARA_PRES(8, 9, 8, 16), ARA_PRES(8, 9, 16, 24),
 };
 
 const Variant* presence_variants_mid(int* n) {

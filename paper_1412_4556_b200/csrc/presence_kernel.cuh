@@ -146,8 +146,9 @@ struct RecBatch {
   }
 
   // occurrence-net loss o = FT2(sum_j FT1(x_j)) of the lane's queued event
+  // s_t1: the FT1 terms as (retention, limit) pairs, one 16-B shared load per column
   __device__ __forceinline__ double row_loss(const LayerParams& p, const double* s_r1, const double* s_l1,
-                                             uint64_t pol_tab, uint32_t rec_s, int lane) const {
+                                             const double2* s_t1, uint64_t pol_tab, uint32_t rec_s, int lane) const {
     cp_async_wait_all();
     const uint4 r = lds_u128(rec_s + 16u * (uint32_t)lane);
     const uint32_t c1 = r.x & 0xffu, c2 = (r.x >> 8) & 0xffu, nz = (r.x >> 16) & 0xffu;
@@ -156,7 +157,7 @@ struct RecBatch {
       if (nz > 2u) {
         constexpr int JP = V * NV;
         const float* row = p.table + (uint64_t)r.w * JP;  // r.w: the record's own event id
-#pragma unroll
+#pragma unroll(NV <= 2 ? NV : 1)  // wide rows: one vector at a time (registers)
         for (int i = 0; i < NV; ++i) {
           float x[V];
           ld_row<V>(row + i * V, pol_tab, x);
@@ -167,15 +168,16 @@ struct RecBatch {
     }
     if (nz <= 2u) {
       // absent columns hold loss 0: clamp(0; R >= 0, L) = +0 exactly, so n < 2 needs no branch
-      sum += clamp_fast((double)__uint_as_float(r.y), s_r1[c1], s_l1[c1]);  // steps 1-2: FT1, sum over ELTs
-      sum += clamp_fast((double)__uint_as_float(r.z), s_r1[c2], s_l1[c2]);
+      const double2 ta = s_t1[c1], tb = s_t1[c2];
+      sum += clamp_fast((double)__uint_as_float(r.y), ta.x, ta.y);  // steps 1-2: FT1, sum over ELTs
+      sum += clamp_fast((double)__uint_as_float(r.z), tb.x, tb.y);
     }
     return clamp_fast(sum, p.r2, p.l2);  // step 3: FT2 (exactly +0 for an empty record)
   }
 };
 
 template <int V, int NV, int G, bool kRec>
-struct BatchOf {
+struct BatchOf {  // G > 1: full-row batches (round by round for wide rows)
   using type = RowBatch<V, NV, G>;
 };
 template <int V, int NV>
@@ -219,13 +221,14 @@ template <int V, int NV, int G, int NW, bool OLT>
 __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_constant__ LayerParams p) {
   constexpr int JP = V * NV;
   constexpr unsigned FULL = 0xffffffffu;
-  constexpr bool kCarry = (G == 1) && RowBatch<V, NV, G>::kAsync;  // narrow rows: records + carried queue
+  constexpr bool kCarry = (G == 1);  // one lane per row: sparse records + carried queue (any row width)
   using Batch = typename BatchOf<V, NV, G, kCarry>::type;
   extern __shared__ uint32_t smem[];
   // FT1 terms, padded to the G*NVL*V columns a row group covers (padding: R = 0, L = +inf, so the
   // branch-free FT1 of a padding column -- always loss 0 -- is exactly +0).
   constexpr int JPS = G * ((NV + G - 1) / G) * V;
   __shared__ double s_r1[JPS], s_l1[JPS];
+  __shared__ double2 s_t1[kCarry ? JPS : 1];  // narrow rows: FT1 as (R, L) pairs, one 16-B load per column
   __shared__ WarpTrials s_wt[NW];
   uint32_t* bits = smem;  // [present_words], already folded by the host (fold_mul)
   const int warp = threadIdx.x >> 5;
@@ -240,12 +243,11 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   for (int j = threadIdx.x; j < JPS; j += blockDim.x) {
     s_r1[j] = j < JP ? p.r1[j] : 0.0;
     s_l1[j] = j < JP ? p.l1[j] : __longlong_as_double(0x7ff0000000000000ll);
+    if constexpr (kCarry) s_t1[j] = make_double2(s_r1[j], s_l1[j]);
   }
   for (uint32_t w = threadIdx.x; w < p.present_words; w += blockDim.x) bits[w] = __ldg(p.present + w);
-  if (lane == 0) {
-    wt.state[0] = wt.state[1] = 0u;
-    wt.bad = 0u;
-  }
+  wt.state[0] = wt.state[1] = 0u;
+  wt.bad = 0u;
   __syncthreads();
 
   const uint64_t pol_tab = make_policy(true, p.l2_hints);
@@ -288,9 +290,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       S0 = 0.0;
       M0 = 0.0;
     }
-    __syncwarp();
-    if (lane == 0) wt.state[a] = 0u;
-    __syncwarp();
+    wt.state[a] = 0u;  // every lane stores the same value: its own later reads see it
   };
   // Finalize every scanned trial whose hits have all been consumed (stream position `done`).
   auto settle = [&](uint32_t done) {
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   auto consume = [&]() {
     if (bn != 0) {
       if constexpr (kCarry) {
-        const double o = rows.row_loss(p, s_r1, s_l1, pol_tab, rec_s, lane);
+        const double o = rows.row_loss(p, s_r1, s_l1, s_t1, pol_tab, rec_s, lane);
         // Batch lane L holds stream position bstart + L (bstart is a multiple of 32).  It belongs to
         // trial 0 if that trial is open and the position lies in its range, else to trial 1 (every
         // queued hit belongs to one of the two open trials).  Each lane accumulates its own hits: no
@@ -354,7 +354,8 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   };
   // Scan one window: lane l holds window positions 4l .. 4l+3 (ids v); CHECKED windows mask positions
   // outside the trial (r = window position of id 0 relative to the trial start, len = trial length).
-  auto scan = [&](const uint4 v, auto checked, uint32_t r, uint32_t len) {
+  // `valid`: all ones, or 0 for a lane whose 4 slots all lie outside the trial (lane-masked tail).
+  auto scan = [&](const uint4 v, auto checked, uint32_t r, uint32_t len, uint32_t valid) {
     const uint32_t id[4] = {v.x, v.y, v.z, v.w};
     uint32_t x[4], wd[4];
 #pragma unroll
@@ -366,8 +367,8 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     // Append the hits in a fixed order that depends only on the window: per pair of slots, first the
     // lanes' first hit of the pair (lanes ascending), then -- only if some lane hit both -- the
     // second ids of those lanes.  One ballot per pair instead of one per slot.
-    pair_insert(wd[0], x[0], id[0], wd[1], x[1], id[1], lt, qt);
-    pair_insert(wd[2], x[2], id[2], wd[3], x[3], id[3], lt, qt);
+    pair_insert(wd[0], x[0], id[0], wd[1], x[1], id[1], lt, qt, valid);
+    pair_insert(wd[2], x[2], id[2], wd[3], x[3], id[3], lt, qt, valid);
     // warp-uniform; at most 31 + 128 = 159 < kQueue queued
     while (qt - q_s >= 128u) issue(32);
   };
@@ -376,13 +377,10 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   for (uint64_t t = (uint64_t)blockIdx.x * NW + warp; t < p.num_trials; t += (uint64_t)gridDim.x * NW, ++k) {
     const int par = (int)(k & 1u);
     if (wt.state[par] != 0u) flush();  // trial k-2 still has hits in flight
-    __syncwarp();
-    if (lane == 0) {
-      wt.trial[par] = t;
-      wt.first[par] = issued + ((qt - q_s) >> 2);  // stream position of the trial's first hit
-      wt.state[par] = 1u;
-    }
-    __syncwarp();
+    // warp-uniform bookkeeping: every lane stores the same values (no lane-0 branch, no syncwarps)
+    wt.trial[par] = t;
+    wt.first[par] = issued + ((qt - q_s) >> 2);  // stream position of the trial's first hit
+    wt.state[par] = 1u;
 
     uint64_t b, e;
     if (p.offsets) {
@@ -434,24 +432,32 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       uint32_t rem = wf1 - 1u;  // full windows after the one in wa
       while (true) {
         if (rem != 0u) wb = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp + 32));
-        scan(wa, BoolC<false>{}, 0u, 0u);
+        scan(wa, BoolC<false>{}, 0u, 0u, 0xffffffffu);
         if (rem == 0u) break;
         --rem;
         lp += 64;
         if (rem != 0u) wa = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp));
-        scan(wb, BoolC<false>{}, 0u, 0u);
+        scan(wb, BoolC<false>{}, 0u, 0u, 0xffffffffu);
         if (rem == 0u) break;
         --rem;
       }
       w = wf1;
     }
-    for (; w < nwin; ++w) scan(load_checked(w), BoolC<true>{}, rel0(w), len);  // tail (or unaligned trial)
-    __syncwarp();
-    if (lane == 0) {
-      wt.end[par] = issued + ((qt - q_s) >> 2);
-      wt.state[par] = 2u;
+    if (vec && (len & 3u) == 0u) {
+      // aligned trial whose length is a multiple of 4: the tail window is whole 16-B vectors, lanes past
+      // the end masked as a unit (no per-slot checks)
+      for (; w < nwin; ++w) {
+        const uint32_t r = rel0(w);
+        const bool ok = r < len;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (ok) v = ld_ids4_stream(p.ids + b + r);
+        scan(v, BoolC<false>{}, 0u, 0u, ok ? 0xffffffffu : 0u);
+      }
+    } else {
+      for (; w < nwin; ++w) scan(load_checked(w), BoolC<true>{}, rel0(w), len, 0xffffffffu);  // tail (or unaligned trial)
     }
-    __syncwarp();
+    wt.end[par] = issued + ((qt - q_s) >> 2);
+    wt.state[par] = 2u;
     if (!kCarry) {
       flush();  // wide rows: one trial at a time (finalized by the flush's settle)
     } else if (bn == 0) {

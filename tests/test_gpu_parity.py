@@ -356,9 +356,19 @@ def test_trials_with_hit_counts_at_batch_boundaries(cuda_device, J, C):
 
 
 def test_automatic_kernel_choice(cuda_device):
-    """ARA_OPT_KERNEL auto: presence kernel for the paper-shaped layer (sparse bitmap), dense kernel when the
-    folded bitmap would send most occurrences to the gather (10M-event catalogue, 100 ELTs)."""
-    for name, want in (("T", ara.KERNEL_PRESENCE), ("P", ara.KERNEL_PRESENCE), ("X", ara.KERNEL_DENSE)):
+    """ARA_OPT_KERNEL auto: presence kernel for the paper-shaped layer (sparse bitmap) and for the stress
+    layer (10M-event catalogue, 100 ELTs: the folded bitmap sends ~48% of the occurrences to the gather,
+    each fetching a 16-B sparse record instead of its 416-B row); dense kernel when most rows hold more
+    than two losses and nearly every occurrence would be gathered."""
+    rng = np.random.default_rng(3)
+    C = 50_000
+    dense_elts = [ara.Elt(np.sort(rng.choice(np.arange(1, C + 1, dtype=np.uint32), int(0.9 * C), replace=False)),
+                          rng.uniform(1.0, 100.0, int(0.9 * C)).astype(np.float32)) for _ in range(8)]
+    ctx = ara.Context(C, dense_elts, [ara.Layer(list(range(8)))])
+    st = ctx.ara_layer_stats(0)
+    assert st["kernel"] == ara.KERNEL_DENSE and st["est_hit_rate"] > 0.9, st
+    ctx.close()
+    for name, want in (("T", ara.KERNEL_PRESENCE), ("P", ara.KERNEL_PRESENCE), ("X", ara.KERNEL_PRESENCE)):
         cfg = synth.Config.load(name)
         ctx = ara.context_for_config(cfg, synth.make_elts(cfg))
         st = ctx.ara_layer_stats(0)
