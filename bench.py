@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--block", type=int, default=None)
     ap.add_argument("--bps", type=int, default=None)
     ap.add_argument("--l2-policy", type=int, default=None)
+    ap.add_argument("--filter", type=int, default=None, choices=[-1, 0, 1],
+                    help="ARA_OPT_FILTER: exact filter stage of the record presence kernel (-1 auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cold", action="store_true")
@@ -253,6 +255,8 @@ def main():
         ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, args.bps)
     if args.l2_policy is not None:
         ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, args.l2_policy)
+    if args.filter is not None:
+        ctx.ara_set_option(ara.ARA_OPT_FILTER, args.filter)
     info = [ctx.ara_layer_info(l) for l in range(L)]
 
     # ---- this rank's YET shard, generated in HBM

@@ -96,6 +96,7 @@ struct ara_ctx {
   int blocks_per_sm = 0;
   int l2_policy = 0;
   int prefetch = 1;
+  int filter = -1;  // ARA_OPT_FILTER: -1 auto, 0 off, 1 on
   int variant = 0;
   int kernel = -1;  // KernelKind, or -1 = per-layer automatic choice
   int persist_max = 0, window_max = 0;
@@ -296,6 +297,7 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   }
   int threads = c->block_threads;
   size_t dyn_smem = 0;
+  KernelFn fn = olt ? var->fn_olt : var->fn;
   if (var->kind == KIND_PRESENCE) {
     threads = var->NW * 32;
     cudaFuncAttributes fa;
@@ -316,11 +318,15 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
     }
     p.present = L.folded;
     p.rec = L.rec;
+    p.exact = L.present;
     p.present_words = fw;
     p.fold_mul = mul;
     dyn_smem = (size_t)fw * 4 + presence_warp_smem(var);
-    ARA_CUDA(cudaFuncSetAttribute((const void*)var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
-    ARA_CUDA(cudaFuncSetAttribute((const void*)var->fn_olt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
+    // exact filter stage (ARA_OPT_FILTER): only on request -- it cuts the DRAM traffic of a folded
+    // bitmap's false positives but measured slower on config X (presence_kernel.cuh, FX)
+    const bool fx = var->fn_fx && c->filter == 1;
+    fn = fx ? (olt ? var->fn_fx_olt : var->fn_fx) : fn;
+    ARA_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
   }
   int bps = c->blocks_per_sm;
   if (bps <= 0) {
@@ -350,7 +356,7 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  ARA_CUDA(cudaLaunchKernelEx(&cfg, olt ? var->fn_olt : var->fn, p));
+  ARA_CUDA(cudaLaunchKernelEx(&cfg, fn, p));
   return ARA_OK;
 }
 
@@ -810,6 +816,10 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
       if (v < 0 || v > 1) return set_error(ARA_E_ARG, "prefetch in {0, 1}");
       c->prefetch = (int)v;
       return ARA_OK;
+    case ARA_OPT_FILTER:
+      if (v < -1 || v > 1) return set_error(ARA_E_ARG, "filter in {-1, 0, 1}");
+      c->filter = (int)v;
+      return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }
@@ -823,6 +833,7 @@ ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
     case ARA_OPT_VARIANT: *v = c->variant; return ARA_OK;
     case ARA_OPT_KERNEL: *v = c->kernel; return ARA_OK;
     case ARA_OPT_PREFETCH: *v = c->prefetch; return ARA_OK;
+    case ARA_OPT_FILTER: *v = c->filter; return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }

@@ -47,7 +47,8 @@ struct LayerParams {
                              // umulhi(x, fold_mul) is set if row e holds a non-zero loss; x = C: sentinel
   uint32_t present_words;    // words of the folded bitmap (staged in shared memory)
   uint32_t fold_mul;         // 2^27 (no folding: word x >> 5) or floor((present_words * 2^32 - 1) / C)
-  const uint4* rec;          // per-event sparse row record (presence kernel, rows <= 16 columns)
+  const uint4* rec;          // per-event sparse row record (presence kernels with one lane per row)
+  const uint32_t* exact;     // UNFOLDED presence bitmap (bit e of word e >> 5), for the FX filter stage
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
 

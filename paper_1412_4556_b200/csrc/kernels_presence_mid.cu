@@ -7,17 +7,22 @@ namespace ara {
 #define ARA_PRES(V_, NV_, G_, NW_) \
   {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, G_, 0, NW_, ara_presence_kernel<V_, NV_, G_, NW_, false>, \
    "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",NW=" #NW_ ">", ara_presence_kernel<V_, NV_, G_, NW_, true>}
+// default one-lane-per-row variant, also instantiated with the exact filter stage (FX)
+#define ARA_PRES_FX(V_, NV_, NW_) \
+  {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, 1, 0, NW_, ara_presence_kernel<V_, NV_, 1, NW_, false>, \
+   "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=1,NW=" #NW_ ">", ara_presence_kernel<V_, NV_, 1, NW_, true>, \
+   ara_presence_kernel<V_, NV_, 1, NW_, false, true>, ara_presence_kernel<V_, NV_, 1, NW_, true, true>}
 
 
 static const Variant kTable[] = {
     // first per row width = default: one lane per row with sparse records (G = 1); then full-row batches
-    ARA_PRES(8, 3, 1, 32), ARA_PRES(8, 3, 2, 16), ARA_PRES(8, 3, 4, 16), ARA_PRES(8, 3, 2, 24),
-    ARA_PRES(8, 4, 1, 32), ARA_PRES(8, 4, 2, 16), ARA_PRES(8, 4, 4, 16), ARA_PRES(8, 4, 2, 24),
-    ARA_PRES(8, 5, 1, 32), ARA_PRES(8, 5, 16, 16), ARA_PRES(8, 5, 8, 16), ARA_PRES(8, 5, 16, 24),
-    ARA_PRES(8, 6, 1, 32), ARA_PRES(8, 6, 16, 16), ARA_PRES(8, 6, 8, 16), ARA_PRES(8, 6, 16, 24),
-    ARA_PRES(8, 7, 1, 32), ARA_PRES(8, 7, 16, 16), ARA_PRES(8, 7, 8, 16), ARA_PRES(8, 7, 16, 24),
-    ARA_PRES(8, 8, 1, 32), ARA_PRES(8, 8, 16, 16), ARA_PRES(8, 8, 8, 16), ARA_PRES(8, 8, 16, 24),
-    ARA_PRES(8, 9, 1, 32), ARA_PRES(8, 9, 16, 16), ARA_PRES(8, 9, 8, 16), ARA_PRES(8, 9, 16, 24),
+    ARA_PRES_FX(8, 3, 32), ARA_PRES(8, 3, 2, 16), ARA_PRES(8, 3, 4, 16), ARA_PRES(8, 3, 2, 24),
+    ARA_PRES_FX(8, 4, 32), ARA_PRES(8, 4, 2, 16), ARA_PRES(8, 4, 4, 16), ARA_PRES(8, 4, 2, 24),
+    ARA_PRES_FX(8, 5, 32), ARA_PRES(8, 5, 16, 16), ARA_PRES(8, 5, 8, 16), ARA_PRES(8, 5, 16, 24),
+    ARA_PRES_FX(8, 6, 32), ARA_PRES(8, 6, 16, 16), ARA_PRES(8, 6, 8, 16), ARA_PRES(8, 6, 16, 24),
+    ARA_PRES_FX(8, 7, 32), ARA_PRES(8, 7, 16, 16), ARA_PRES(8, 7, 8, 16), ARA_PRES(8, 7, 16, 24),
+    ARA_PRES_FX(8, 8, 32), ARA_PRES(8, 8, 16, 16), ARA_PRES(8, 8, 8, 16), ARA_PRES(8, 8, 16, 24),
+    ARA_PRES_FX(8, 9, 32), ARA_PRES(8, 9, 16, 16), ARA_PRES(8, 9, 8, 16), ARA_PRES(8, 9, 16, 24),
 };
 
 const Variant* presence_variants_mid(int* n) {

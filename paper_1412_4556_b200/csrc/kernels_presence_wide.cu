@@ -7,17 +7,22 @@ namespace ara {
 #define ARA_PRES(V_, NV_, G_, NW_) \
   {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, G_, 0, NW_, ara_presence_kernel<V_, NV_, G_, NW_, false>, \
    "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",NW=" #NW_ ">", ara_presence_kernel<V_, NV_, G_, NW_, true>}
+// default one-lane-per-row variant, also instantiated with the exact filter stage (FX)
+#define ARA_PRES_FX(V_, NV_, NW_) \
+  {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, 1, 0, NW_, ara_presence_kernel<V_, NV_, 1, NW_, false>, \
+   "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=1,NW=" #NW_ ">", ara_presence_kernel<V_, NV_, 1, NW_, true>, \
+   ara_presence_kernel<V_, NV_, 1, NW_, false, true>, ara_presence_kernel<V_, NV_, 1, NW_, true, true>}
 
 
 static const Variant kTable[] = {
     // first per row width = default: one lane per row with sparse records (G = 1); then full-row batches
-    ARA_PRES(8, 10, 1, 32), ARA_PRES(8, 10, 16, 16), ARA_PRES(8, 10, 8, 16), ARA_PRES(8, 10, 16, 24),
-    ARA_PRES(8, 11, 1, 32), ARA_PRES(8, 11, 16, 16), ARA_PRES(8, 11, 8, 16), ARA_PRES(8, 11, 16, 24),
-    ARA_PRES(8, 12, 1, 32), ARA_PRES(8, 12, 16, 16), ARA_PRES(8, 12, 8, 16), ARA_PRES(8, 12, 16, 24),
-    ARA_PRES(8, 13, 1, 32), ARA_PRES(8, 13, 16, 16), ARA_PRES(8, 13, 8, 16), ARA_PRES(8, 13, 16, 24),
-    ARA_PRES(8, 14, 1, 32), ARA_PRES(8, 14, 16, 16), ARA_PRES(8, 14, 8, 16), ARA_PRES(8, 14, 16, 24),
-    ARA_PRES(8, 15, 1, 32), ARA_PRES(8, 15, 16, 16), ARA_PRES(8, 15, 8, 16), ARA_PRES(8, 15, 16, 24),
-    ARA_PRES(8, 16, 1, 32), ARA_PRES(8, 16, 16, 16), ARA_PRES(8, 16, 8, 16), ARA_PRES(8, 16, 16, 24),
+    ARA_PRES_FX(8, 10, 32), ARA_PRES(8, 10, 16, 16), ARA_PRES(8, 10, 8, 16), ARA_PRES(8, 10, 16, 24),
+    ARA_PRES_FX(8, 11, 32), ARA_PRES(8, 11, 16, 16), ARA_PRES(8, 11, 8, 16), ARA_PRES(8, 11, 16, 24),
+    ARA_PRES_FX(8, 12, 32), ARA_PRES(8, 12, 16, 16), ARA_PRES(8, 12, 8, 16), ARA_PRES(8, 12, 16, 24),
+    ARA_PRES_FX(8, 13, 32), ARA_PRES(8, 13, 16, 16), ARA_PRES(8, 13, 8, 16), ARA_PRES(8, 13, 16, 24),
+    ARA_PRES_FX(8, 14, 32), ARA_PRES(8, 14, 16, 16), ARA_PRES(8, 14, 8, 16), ARA_PRES(8, 14, 16, 24),
+    ARA_PRES_FX(8, 15, 32), ARA_PRES(8, 15, 16, 16), ARA_PRES(8, 15, 8, 16), ARA_PRES(8, 15, 16, 24),
+    ARA_PRES_FX(8, 16, 32), ARA_PRES(8, 16, 16, 16), ARA_PRES(8, 16, 8, 16), ARA_PRES(8, 16, 16, 24),
 };
 
 const Variant* presence_variants_wide(int* n) {

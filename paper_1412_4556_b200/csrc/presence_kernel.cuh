@@ -217,11 +217,20 @@ struct BoolC {
 // the sharding or the launch shape.
 // OLT: also track the largest occurrence-net loss per trial (ara_run_ex); a separate instantiation so
 // the plain YLT path carries no extra registers.
-template <int V, int NV, int G, int NW, bool OLT>
+// FX (one lane per row only): EXACT filter stage for layers whose sparse records do not stay in L2.  A
+// batch of queued candidates first loads, per lane, the word of the layer's unfolded presence bitmap
+// (global memory, (C+1) bits, L2-resident) that holds its event; one batch later only the candidates
+// whose exact bit is set fetch their record, the others (false positives of the fold) get a zero record
+// in shared memory.  A zero record gives o = +0, exactly what their own (zero) record gave, so the results
+// are bitwise identical with and without FX; only the records' DRAM traffic changes.  Measured on config
+// X (B200): DRAM traffic 301 -> 74 GB per 8M trials, but 6.6 instead of 5.9 ms per 1M trials (the extra
+// L2 round trip per batch and its shared-memory dependencies), so it is an option, off by default.
+template <int V, int NV, int G, int NW, bool OLT, bool FX = false>
 __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_constant__ LayerParams p) {
   constexpr int JP = V * NV;
   constexpr unsigned FULL = 0xffffffffu;
   constexpr bool kCarry = (G == 1);  // one lane per row: sparse records + carried queue (any row width)
+  static_assert(!FX || kCarry, "the exact filter stage needs record batches");
   using Batch = typename BatchOf<V, NV, G, kCarry>::type;
   extern __shared__ uint32_t smem[];
   // FT1 terms, padded to the G*NVL*V columns a row group covers (padding: R = 0, L = +inf, so the
@@ -266,6 +275,9 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   Batch rows;
   uint32_t bstart = 0;           // pending batch: stream position of slot 0
   int bn = 0;                    // pending batch size (0 = none)
+  uint32_t f_id = 0, f_w = 0;    // FX: this lane's candidate of the filter batch and its exact bitmap word
+  uint32_t fstart = 0;           // FX: stream position of the filter batch's slot 0
+  int fn = 0;                    // FX: filter batch size (0 = none)
   unsigned bad = 0;
 
   // FT3 on the warp-combined sum of parity slot a; lane 0 writes the YLT.
@@ -322,16 +334,35 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       }
       bn = 0;
     }
-    settle(issued);  // every issued hit is consumed now
+    settle((FX && fn != 0) ? fstart : issued);  // every hit before the filter batch is consumed now
   };
   // Issue the next n (<= 32) queued hits as a batch (consuming the previous batch first).
   auto issue = [&](int n) {
     consume();
     __syncwarp();
+    if constexpr (FX) {  // filter batch -> record batch: records only for exact hits
+      if (fn != 0) {
+        const uint32_t xe = f_id;  // 0 for empty slots and invalid ids
+        const bool tp = (f_w >> (xe & 31u)) & 1u;
+        if (tp) {
+          cp_async16(rec_s + 16u * (uint32_t)lane, p.rec + xe, pol_tab);
+        } else {  // (fetching row 0's zero record instead makes one L2 sector a hot spot: 15x slower on X)
+          asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" :: "r"(rec_s + 16u * (uint32_t)lane), "r"(0u) : "memory");
+        }
+        cp_async_commit();
+        bstart = fstart;
+        bn = fn;
+        fn = 0;
+      }
+      if (n == 0) return;  // flush: nothing left to take from the queue
+    }
     const uint32_t count = (qt - q_s) >> 2;
     const uint32_t e = lane < n ? q[lane] : 1u;
     bad |= (e - 1u >= C) ? 1u : 0u;  // an invalid id reached the queue through the sentinel bit
-    if constexpr (kCarry) {
+    if constexpr (FX) {  // queue -> filter batch: load the exact presence words (used one batch later)
+      f_id = (lane < n && e - 1u < C) ? e : 0u;
+      f_w = f_id != 0u ? ld_id(p.exact + (f_id >> 5), pol_tab) : 0u;
+    } else if constexpr (kCarry) {
       rows.issue(p, q, n, lane, pol_tab, rec_s);
     } else {
       rows.issue(p, q, n, lane, pol_tab, s_r1, s_l1, S0, M0);
@@ -339,8 +370,13 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     __syncwarp();  // every lane has read its batch slots
     for (uint32_t i = (uint32_t)lane; i + (uint32_t)n < count; i += 32u) q[i] = q[i + n];  // n == 32 here
     __syncwarp();
-    bstart = issued;
-    bn = n;
+    if constexpr (FX) {
+      fstart = issued;
+      fn = n;
+    } else {
+      bstart = issued;
+      bn = n;
+    }
     issued += 32u;  // a partial batch skips the rest of its 32 stream positions: batches stay 32-aligned
     qt -= 4u * (uint32_t)n;
     if constexpr (!kCarry) consume();  // wide rows: rows.issue already consumed round by round
@@ -349,6 +385,9 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     while (qt != q_s) {
       const uint32_t count = (qt - q_s) >> 2;
       issue(count < 32 ? (int)count : 32);
+    }
+    if constexpr (FX) {
+      if (fn != 0) issue(0);  // the filter batch becomes the record batch
     }
     consume();
   };
@@ -460,7 +499,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     wt.state[par] = 2u;
     if (!kCarry) {
       flush();  // wide rows: one trial at a time (finalized by the flush's settle)
-    } else if (bn == 0) {
+    } else if (bn == 0 && (!FX || fn == 0)) {
       settle(issued);  // nothing pending: a trial with no outstanding hits is final now
     }
   }

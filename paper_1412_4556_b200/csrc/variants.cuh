@@ -18,6 +18,8 @@ struct Variant {
   KernelFn fn;
   const char* name;
   KernelFn fn_olt;  // the same kernel also producing the occurrence loss table (presence kernels; dense: fn)
+  KernelFn fn_fx = nullptr;      // presence, one lane per row: with the exact filter stage (FX), or nullptr
+  KernelFn fn_fx_olt = nullptr;  // the same with the occurrence loss table
 };
 
 // Defined in kernels_presence.cu / kernels_dense.cu.  First entry per row width is the default.

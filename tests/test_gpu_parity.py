@@ -141,6 +141,39 @@ def test_every_row_width_bitwise(cuda_device, J):
         assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, kernel=k, variant=v), want), (k, v)
 
 
+@pytest.mark.parametrize("J", [2, 16, 100])
+def test_exact_filter_stage_bitwise(cuda_device, J):
+    """ARA_OPT_FILTER: with a folded bitmap (3M-event catalogue > the shared-memory bitmap) the exact filter
+    stage fetches records only for true hits and gives false positives a zero record; the YLT (and the
+    occurrence loss table) must equal the oracle bitwise with the stage forced on, forced off and auto, for
+    fixed and ragged trials.  Also forced on for an unfolded bitmap."""
+    for C, n in ((3_000_000, 20_000), (5000, 300)):
+        Cc, elts, layer, yet, N, K = _small_problem(J, C=C, n=n, K=1000 if C > 5000 else 37,
+                                                    N=300 if C > 5000 else 333)
+        want = oracle.ylt(Cc, yet, None, N, K, elts, [layer])
+        rng = np.random.default_rng(J)
+        lens = rng.integers(0, 1500, size=200)
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+        ryet = yet[: int(off[-1])] if off[-1] <= yet.size else np.resize(yet, int(off[-1]))
+        rwant = oracle.ylt(Cc, ryet, off, len(lens), 0, elts, [layer])
+        ctx = _ctx_from(Cc, elts, [layer])
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+        for f in (1, 0, -1):
+            ctx.ara_set_option(ara.ARA_OPT_FILTER, f)
+            assert np.array_equal(gpu_ylt(None, ctx, yet, K=K), want), (C, f)
+            assert np.array_equal(gpu_ylt(None, ctx, ryet, offsets_np=off), rwant), (C, f, "ragged")
+        ctx.ara_set_option(ara.ARA_OPT_FILTER, 1)
+        dev = torch.device("cuda:0")
+        ids = torch.from_numpy(yet.view(np.int32)).to(dev)
+        ylt = torch.empty((1, N), dtype=torch.float64, device=dev)
+        olt = torch.empty((1, N), dtype=torch.float64, device=dev)
+        ctx.ara_run_ex(ids, ylt, olt, events_per_trial=K, num_trials=N)
+        ctx.ara_check()
+        assert np.array_equal(ylt.cpu().numpy(), want)
+        assert np.array_equal(olt.cpu().numpy(), oracle.ylt_olt(Cc, yet, None, N, K, elts, [layer])[1]), (C, "olt")
+        ctx.close()
+
+
 @pytest.mark.parametrize("kw", [dict(inf_limits=True), dict(zero_ret=True), dict(zero_ret=True, inf_limits=True),
                                 dict(empty_elts=(0, 2)), dict(integer=False)])
 def test_term_edge_cases(cuda_device, kw):
