@@ -480,6 +480,30 @@ def main():
                          "served mostly from DRAM (ncu: L2 hit ~36%)"}
         ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_AUTO)
         ctx.ara_check(stream)
+    # ---- SURVEY N3 ablation: the precombined occurrence-net table o[e] (no ELT lookups at run time),
+    # timed beside; its YLT must equal the product path's bit for bit (checked here)
+    pre = None
+    if not args.profile and args.variant is None and kernel_name == "ara_presence_kernel":
+        ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        ref_ylt = ylt_local.clone()  # the product path's YLT
+        ctx.ara_set_option(ara.ARA_OPT_PRECOMBINED, 1)
+        for _ in range(2):
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        npc = 5
+        for _ in range(npc):
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        pms = a.elapsed_time(b) / npc / L
+        same = bool(torch.equal(ylt_local, ref_ylt))
+        ctx.ara_set_option(ara.ARA_OPT_PRECOMBINED, 0)
+        ctx.ara_check(stream)
+        pre = {"launch_ms": pms, "ylt_bitwise_equal": same,
+               "note": "SURVEY.md 8(f) N3 ablation: per-layer table o[e] = FT2(sum_j FT1(l_ej)) built once; a hit "
+                       "gathers one 8-B value and does no FT1/FT2 work.  Exact for deterministic losses only; "
+                       "performs no ELT lookups at run time, so it is not the headline"}
     lookups_exact = float(sum(len(l.elts) for l in cfg.layers)) * (
         N * cfg.kmin if cfg.fixed_length else float(synth.trial_offsets(cfg.seed, N, cfg.kmin, cfg.kmax)[-1]))
     value = ms_per_step * 1e6 / N
@@ -508,6 +532,7 @@ def main():
                      "effective_GBps_68B": dense_bytes / (launch_ms * 1e-3) / 1e9,
                      "note": alg_note + f"; peak {peak_src}"},
         "dense_kernel": dense,
+        "precombined_N3": pre,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps * (L + n_metric_launches),

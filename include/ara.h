@@ -218,6 +218,12 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           bitmap against the layer's unfolded presence bitmap (global memory,
  *                           L2-resident) before fetching its record: 4x less DRAM traffic on config X,
  *                           but measured slower there, hence off.  Identical results either way.
+ *   ARA_OPT_PRECOMBINED     0 (default) or 1: ablation of SURVEY.md 8(f) N3.  Steps 1-3 depend only on
+ *                           the event, so the presence kernel may gather a per-layer table
+ *                           o[e] = FT2(sum_j FT1(l_ej)) (fp64, (C+1) x 8 B, built on the first run
+ *                           with the option set) instead of the sparse records.  Bitwise identical
+ *                           YLT; exact only for deterministic losses (no secondary uncertainty,
+ *                           PAPER.md:125), and no ELT lookups happen at run time.
  * ARA_OPT_BLOCK_THREADS applies to the dense kernel; the presence kernel fixes its block size. */
 typedef enum {
   ARA_OPT_BLOCK_THREADS = 1,
@@ -226,7 +232,8 @@ typedef enum {
   ARA_OPT_VARIANT = 4,
   ARA_OPT_KERNEL = 5,
   ARA_OPT_PREFETCH = 6,
-  ARA_OPT_FILTER = 7
+  ARA_OPT_FILTER = 7,
+  ARA_OPT_PRECOMBINED = 8
 } ara_option;
 ARA_API ara_status ara_set_option(ara_ctx* ctx, ara_option opt, int64_t value);
 ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);

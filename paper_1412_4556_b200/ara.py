@@ -24,6 +24,7 @@ ARA_OK, ARA_E_ARG, ARA_E_RANGE, ARA_E_DUP, ARA_E_VALUE, ARA_E_NOMEM, ARA_E_CUDA,
 ARA_OPT_BLOCK_THREADS, ARA_OPT_BLOCKS_PER_SM, ARA_OPT_L2_POLICY, ARA_OPT_VARIANT, ARA_OPT_KERNEL = 1, 2, 3, 4, 5
 ARA_OPT_PREFETCH = 6
 ARA_OPT_FILTER = 7
+ARA_OPT_PRECOMBINED = 8
 KERNEL_AUTO, KERNEL_PRESENCE, KERNEL_DENSE = -1, 0, 1
 STUDY_INTERLEAVED, STUDY_INDEPENDENT, STUDY_SORTED = 0, 1, 2
 ARA_MAX_ELTS_PER_LAYER = 128

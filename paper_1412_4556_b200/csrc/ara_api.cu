@@ -68,6 +68,7 @@ struct Layer {
   uint32_t folded_words = 0;    // words of the current fold (0: not built yet)
   uint32_t fold_mul = 0;        // its multiplier (LayerParams::fold_mul)
   uint4* rec = nullptr;         // sparse row records (C + 1) x 16 B (presence kernels with one lane per row)
+  double* occ = nullptr;        // precombined o[e] per event, (C + 1) x 8 B, built on first use
   // Section IV.B study structures, built on first use by ara_run_study
   float* indep = nullptr;         // J x (C + 1) independent per-ELT direct-access arrays
   uint32_t* sorted_ids = nullptr; // per-ELT (event, loss) pairs sorted by event
@@ -97,6 +98,7 @@ struct ara_ctx {
   int l2_policy = 0;
   int prefetch = 1;
   int filter = -1;  // ARA_OPT_FILTER: -1 auto, 0 off, 1 on
+  int precombined = 0;  // ARA_OPT_PRECOMBINED: 1 = gather o[e] from the precombined table
   int variant = 0;
   int kernel = -1;  // KernelKind, or -1 = per-layer automatic choice
   int persist_max = 0, window_max = 0;
@@ -223,6 +225,22 @@ __global__ void __launch_bounds__(256) record_build_kernel(uint4* __restrict__ r
   }
 }
 
+// o[e] = FT2(sum_j FT1(T[e][j])) per event, summed over the layer's columns in order with the
+// kernels' clamp (absent losses give exact +0 terms), so it equals the record path's value bit for bit.
+__global__ void __launch_bounds__(256) occ_build_kernel(double* __restrict__ occ, const float* __restrict__ table,
+                                                        uint32_t jpad, const __grid_constant__ LayerParams p,
+                                                        uint64_t rows) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows; e += (uint64_t)gridDim.x * blockDim.x) {
+    const float* row = table + e * jpad;
+    double sum = 0.0;
+    for (uint32_t j = 0; j < jpad; ++j) {
+      const float x = row[j];
+      if (x != 0.0f) sum += clamp_fast((double)x, p.r1[j], p.l1[j]);
+    }
+    occ[e] = clamp_fast(sum, p.r2, p.l2);
+  }
+}
+
 static void destroy_ctx(ara_ctx* c) {
   if (!c) return;
   DeviceGuard guard(c->device);
@@ -232,6 +250,7 @@ static void destroy_ctx(ara_ctx* c) {
     cudaFree(L.present);
     cudaFree(L.folded);
     cudaFree(L.rec);
+    cudaFree(L.occ);
     cudaFree(L.indep);
     cudaFree(L.sorted_ids);
     cudaFree(L.sorted_loss);
@@ -326,6 +345,20 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
     // bitmap's false positives but measured slower on config X (presence_kernel.cuh, FX)
     const bool fx = var->fn_fx && c->filter == 1;
     fn = fx ? (olt ? var->fn_fx_olt : var->fn_fx) : fn;
+    if (c->precombined && var->fn_pc) {  // SURVEY N3 ablation: o[e] tabulated once per layer
+      if (!L.occ) {
+        if (cudaMalloc(&L.occ, ((size_t)C + 1) * sizeof(double)) != cudaSuccess) {
+          cudaGetLastError();
+          return set_error(ARA_E_NOMEM, "precombined table");
+        }
+        const uint64_t rows = C + 1;
+        const unsigned ob = (unsigned)std::min<uint64_t>((rows + 255) / 256, (uint64_t)c->sms * 16);
+        occ_build_kernel<<<ob, 256, 0, stream>>>(L.occ, L.table, L.jpad, p, rows);
+        ARA_CUDA(cudaGetLastError());
+      }
+      p.occ = L.occ;
+      fn = olt ? var->fn_pc_olt : var->fn_pc;
+    }
     ARA_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
   }
   int bps = c->blocks_per_sm;
@@ -820,6 +853,10 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
       if (v < -1 || v > 1) return set_error(ARA_E_ARG, "filter in {-1, 0, 1}");
       c->filter = (int)v;
       return ARA_OK;
+    case ARA_OPT_PRECOMBINED:
+      if (v < 0 || v > 1) return set_error(ARA_E_ARG, "precombined in {0, 1}");
+      c->precombined = (int)v;
+      return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }
@@ -834,6 +871,7 @@ ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
     case ARA_OPT_KERNEL: *v = c->kernel; return ARA_OK;
     case ARA_OPT_PREFETCH: *v = c->prefetch; return ARA_OK;
     case ARA_OPT_FILTER: *v = c->filter; return ARA_OK;
+    case ARA_OPT_PRECOMBINED: *v = c->precombined; return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }

@@ -49,6 +49,7 @@ struct LayerParams {
   uint32_t fold_mul;         // 2^27 (no folding: word x >> 5) or floor((present_words * 2^32 - 1) / C)
   const uint4* rec;          // per-event sparse row record (presence kernels with one lane per row)
   const uint32_t* exact;     // UNFOLDED presence bitmap (bit e of word e >> 5), for the FX filter stage
+  const double* occ;         // precombined occurrence-net loss FT2(sum_j FT1(l_ej)) per event
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
 
@@ -165,6 +166,9 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
   return v;
 }
 // 16-byte asynchronous global -> shared copy (L2 only), completion awaited with cp_async_wait_all.
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(saddr), "l"(g) : "memory");
+}
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(saddr), "l"(g), "l"(pol) : "memory");
 }

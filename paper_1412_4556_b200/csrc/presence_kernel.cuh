@@ -176,13 +176,39 @@ struct RecBatch {
   }
 };
 
-template <int V, int NV, int G, bool kRec>
+// SURVEY N3 (precombined occurrence-net event table, an ablation): steps 1-3 depend only on the event,
+// so ara_create may tabulate o[e] = FT2(sum_j FT1(l_ej)) per layer (fp64, summed in layer order like the
+// oracle, so bitwise equal to the record path); a hit then moves one 8-B value and does no FT1/FT2
+// work.  Exact for the deterministic method only (secondary uncertainty, would vary the
+// losses per occurrence), and it performs no ELT lookups at run time -- reported separately.
+struct OccBatch {
+  static constexpr bool kAsync = true;
+  __device__ __forceinline__ void issue(const LayerParams& p, const uint32_t* __restrict__ q, int n, int lane,
+                                        uint64_t, uint32_t rec_s) const {
+    const uint32_t e = lane < n ? q[lane] : 0u;
+    cp_async8(rec_s + 16u * (uint32_t)lane, p.occ + (e <= p.C ? e : 0u));  // o[0] = +0
+    cp_async_commit();
+  }
+  __device__ __forceinline__ double row_loss(const LayerParams&, const double*, const double*, const double2*,
+                                             uint64_t, uint32_t rec_s, int lane) const {
+    cp_async_wait_all();
+    double o;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(o) : "r"(rec_s + 16u * (uint32_t)lane) : "memory");
+    return o;
+  }
+};
+
+template <int V, int NV, int G, bool kRec, bool kOcc = false>
 struct BatchOf {  // G > 1: full-row batches (round by round for wide rows)
   using type = RowBatch<V, NV, G>;
 };
 template <int V, int NV>
-struct BatchOf<V, NV, 1, true> {
+struct BatchOf<V, NV, 1, true, false> {
   using type = RecBatch<V, NV>;
+};
+template <int V, int NV>
+struct BatchOf<V, NV, 1, true, true> {
+  using type = OccBatch;
 };
 
 // Per-warp bookkeeping of the (at most two) trials whose hits are still in flight (carried queue).
@@ -225,13 +251,15 @@ struct BoolC {
 // are bitwise identical with and without FX; only the records' DRAM traffic changes.  Measured on config
 // X (B200): DRAM traffic 301 -> 74 GB per 8M trials, but 6.6 instead of 5.9 ms per 1M trials (the extra
 // L2 round trip per batch and its shared-memory dependencies), so it is an option, off by default.
-template <int V, int NV, int G, int NW, bool OLT, bool FX = false>
+// PC: SURVEY N3 ablation -- batches gather the precombined o[e] (OccBatch) instead of records.
+template <int V, int NV, int G, int NW, bool OLT, bool FX = false, bool PC = false>
 __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_constant__ LayerParams p) {
   constexpr int JP = V * NV;
   constexpr unsigned FULL = 0xffffffffu;
   constexpr bool kCarry = (G == 1);  // one lane per row: sparse records + carried queue (any row width)
   static_assert(!FX || kCarry, "the exact filter stage needs record batches");
-  using Batch = typename BatchOf<V, NV, G, kCarry>::type;
+  static_assert(!PC || (kCarry && !FX), "the precombined table replaces the record batches");
+  using Batch = typename BatchOf<V, NV, G, kCarry, PC>::type;
   extern __shared__ uint32_t smem[];
   // FT1 terms, padded to the G*NVL*V columns a row group covers (padding: R = 0, L = +inf, so the
   // branch-free FT1 of a padding column -- always loss 0 -- is exactly +0).
@@ -255,8 +283,10 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     if constexpr (kCarry) s_t1[j] = make_double2(s_r1[j], s_l1[j]);
   }
   for (uint32_t w = threadIdx.x; w < p.present_words; w += blockDim.x) bits[w] = __ldg(p.present + w);
-  wt.state[0] = wt.state[1] = 0u;
-  wt.bad = 0u;
+  if (lane == 0) {
+    wt.state[0] = wt.state[1] = 0u;
+    wt.bad = 0u;
+  }
   __syncthreads();
 
   const uint64_t pol_tab = make_policy(true, p.l2_hints);
@@ -302,7 +332,9 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       S0 = 0.0;
       M0 = 0.0;
     }
-    wt.state[a] = 0u;  // every lane stores the same value: its own later reads see it
+    __syncwarp();
+    if (lane == 0) wt.state[a] = 0u;
+    __syncwarp();
   };
   // Finalize every scanned trial whose hits have all been consumed (stream position `done`).
   auto settle = [&](uint32_t done) {
@@ -416,10 +448,13 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   for (uint64_t t = (uint64_t)blockIdx.x * NW + warp; t < p.num_trials; t += (uint64_t)gridDim.x * NW, ++k) {
     const int par = (int)(k & 1u);
     if (wt.state[par] != 0u) flush();  // trial k-2 still has hits in flight
-    // warp-uniform bookkeeping: every lane stores the same values (no lane-0 branch, no syncwarps)
-    wt.trial[par] = t;
-    wt.first[par] = issued + ((qt - q_s) >> 2);  // stream position of the trial's first hit
-    wt.state[par] = 1u;
+    __syncwarp();
+    if (lane == 0) {  // warp-uniform bookkeeping in shared memory (one writer, then a warp barrier)
+      wt.trial[par] = t;
+      wt.first[par] = issued + ((qt - q_s) >> 2);  // stream position of the trial's first hit
+      wt.state[par] = 1u;
+    }
+    __syncwarp();
 
     uint64_t b, e;
     if (p.offsets) {
@@ -495,8 +530,12 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     } else {
       for (; w < nwin; ++w) scan(load_checked(w), BoolC<true>{}, rel0(w), len, 0xffffffffu);  // tail (or unaligned trial)
     }
-    wt.end[par] = issued + ((qt - q_s) >> 2);
-    wt.state[par] = 2u;
+    __syncwarp();
+    if (lane == 0) {
+      wt.end[par] = issued + ((qt - q_s) >> 2);
+      wt.state[par] = 2u;
+    }
+    __syncwarp();
     if (!kCarry) {
       flush();  // wide rows: one trial at a time (finalized by the flush's settle)
     } else if (bn == 0 && (!FX || fn == 0)) {

@@ -20,6 +20,8 @@ struct Variant {
   KernelFn fn_olt;  // the same kernel also producing the occurrence loss table (presence kernels; dense: fn)
   KernelFn fn_fx = nullptr;      // presence, one lane per row: with the exact filter stage (FX), or nullptr
   KernelFn fn_fx_olt = nullptr;  // the same with the occurrence loss table
+  KernelFn fn_pc = nullptr;      // presence, one lane per row: precombined o[e] table, or nullptr
+  KernelFn fn_pc_olt = nullptr;
 };
 
 // Defined in kernels_presence.cu / kernels_dense.cu.  First entry per row width is the default.

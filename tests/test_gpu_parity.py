@@ -174,6 +174,39 @@ def test_exact_filter_stage_bitwise(cuda_device, J):
         ctx.close()
 
 
+@pytest.mark.parametrize("J", [1, 2, 16, 17, 100])
+def test_precombined_table_bitwise(cuda_device, J):
+    """ARA_OPT_PRECOMBINED (SURVEY N3 ablation): gathering the tabulated o[e] = FT2(sum_j FT1(l_ej)) gives
+    the oracle's YLT and OLT bitwise (integer regime), fixed and ragged trials, and the real regime within
+    tolerance of the oracle and bitwise equal to the record path."""
+    for integer in (True, False):
+        C, elts, layer, yet, N, K = _small_problem(J, integer=integer)
+        want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+        ctx = _ctx_from(C, elts, [layer])
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+        base = gpu_ylt(None, ctx, yet, K=K)
+        ctx.ara_set_option(ara.ARA_OPT_PRECOMBINED, 1)
+        got = gpu_ylt(None, ctx, yet, K=K)
+        assert np.array_equal(got, base), (J, integer)
+        if integer:
+            assert np.array_equal(got, want), J
+            lens = np.random.default_rng(J).integers(0, 200, size=50)
+            off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+            ryet = np.resize(yet, int(off[-1]))
+            assert np.array_equal(gpu_ylt(None, ctx, ryet, offsets_np=off),
+                                  oracle.ylt(C, ryet, off, len(lens), 0, elts, [layer])), (J, "ragged")
+            dev = torch.device("cuda:0")
+            ids = torch.from_numpy(yet.view(np.int32)).to(dev)
+            ylt = torch.empty((1, N), dtype=torch.float64, device=dev)
+            olt = torch.empty((1, N), dtype=torch.float64, device=dev)
+            ctx.ara_run_ex(ids, ylt, olt, events_per_trial=K, num_trials=N)
+            ctx.ara_check()
+            assert np.array_equal(olt.cpu().numpy(), oracle.ylt_olt(C, yet, None, N, K, elts, [layer])[1]), J
+        else:
+            assert np.all(within_tol(got, want)), J
+        ctx.close()
+
+
 @pytest.mark.parametrize("kw", [dict(inf_limits=True), dict(zero_ret=True), dict(zero_ret=True, inf_limits=True),
                                 dict(empty_elts=(0, 2)), dict(integer=False)])
 def test_term_edge_cases(cuda_device, kw):
