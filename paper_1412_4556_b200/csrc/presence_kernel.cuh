@@ -447,15 +447,6 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   uint32_t k = 0;  // local trial counter (parity = k & 1)
   for (uint64_t t = (uint64_t)blockIdx.x * NW + warp; t < p.num_trials; t += (uint64_t)gridDim.x * NW, ++k) {
     const int par = (int)(k & 1u);
-    if (wt.state[par] != 0u) flush();  // trial k-2 still has hits in flight
-    __syncwarp();
-    if (lane == 0) {  // warp-uniform bookkeeping in shared memory (one writer, then a warp barrier)
-      wt.trial[par] = t;
-      wt.first[par] = issued + ((qt - q_s) >> 2);  // stream position of the trial's first hit
-      wt.state[par] = 1u;
-    }
-    __syncwarp();
-
     uint64_t b, e;
     if (p.offsets) {
       b = p.offsets[t];
@@ -469,6 +460,20 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       e = b + p.K;
     }
     const uint32_t len = (uint32_t)(e - b);
+    const bool vec = vec_ok && ((b & 3u) == 0);
+    const uint32_t wf1 = vec ? len / 128u : 0u;  // full windows
+    // the trial's first full window is requested before the bookkeeping below, so its latency overlaps it
+    uint4 wfirst = make_uint4(0u, 0u, 0u, 0u);
+    if (wf1 != 0u) wfirst = ld_ids4_stream(reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint4*>(p.ids + b) + lane));
+    if (wt.state[par] != 0u) flush();  // trial k-2 still has hits in flight
+    __syncwarp();
+    if (lane == 0) {  // warp-uniform bookkeeping in shared memory (one writer, then a warp barrier)
+      wt.trial[par] = t;
+      wt.first[par] = issued + ((qt - q_s) >> 2);  // stream position of the trial's first hit
+      wt.state[par] = 1u;
+    }
+    __syncwarp();
+
     // Bring this warp's NEXT trial into L2 (lane l prefetches its 128-B line l: the first 4 KB), so its
     // windows arrive at L2 latency: one window of register prefetch cannot cover DRAM latency.
     if (p.prefetch) {
@@ -485,9 +490,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     // trial start is 16-B aligned, full windows are single 16-B vectors streamed through a running
     // per-lane pointer with no checks, one window held ahead in registers; the last partial window (or
     // an unaligned trial) goes through the checked loader.
-    const bool vec = vec_ok && ((b & 3u) == 0);
     const uint32_t nwin = (len + 127u) / 128u;
-    const uint32_t wf1 = vec ? len / 128u : 0u;  // full windows
     auto load_checked = [&](uint32_t w) -> uint4 {
       const uint32_t r = w * 128u + 4u * lane;  // trial position of this lane's first slot
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     uint32_t w = 0;
     if (wf1 != 0u) {  // full windows: running pointer, one window held ahead (two register sets, unrolled)
       const uint4* lp = reinterpret_cast<const uint4*>(p.ids + b) + lane;
-      uint4 wa = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp)), wb;
+      uint4 wa = wfirst, wb;
       uint32_t rem = wf1 - 1u;  // full windows after the one in wa
       while (true) {
         if (rem != 0u) wb = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp + 32));
