@@ -218,6 +218,7 @@ struct WarpTrials {
   uint32_t end[2];    // stream position one past its last hit (valid once its scan is done)
   uint32_t state[2];  // 0 free, 1 scanning, 2 scanned (waiting for its hits to be consumed)
   uint32_t bad;
+  uint32_t cur;       // parity of the most recently started trial
 };
 
 template <bool B>
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   if (lane == 0) {
     wt.state[0] = wt.state[1] = 0u;
     wt.bad = 0u;
+    wt.cur = 0u;
   }
   __syncthreads();
 
@@ -347,13 +349,14 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     if (bn != 0) {
       if constexpr (kCarry) {
         const double o = rows.row_loss(p, s_r1, s_l1, s_t1, pol_tab, rec_s, lane);
-        // Batch lane L holds stream position bstart + L (bstart is a multiple of 32).  It belongs to
-        // trial 0 if that trial is open and the position lies in its range, else to trial 1 (every
-        // queued hit belongs to one of the two open trials).  Each lane accumulates its own hits: no
+        // Batch lane L holds stream position bstart + L (bstart is a multiple of 32).  A queued hit
+        // belongs to the most recently started trial (parity wt.cur) if it lies at or after that
+        // trial's first hit, else to its predecessor (the other parity): the trial before that was
+        // fully consumed when the current one started.  Each lane accumulates its own hits: no
         // shuffles per batch (finalize rotates once per trial).
-        const uint32_t st0 = wt.state[0];
-        const uint32_t len0 = (st0 == 2u ? wt.end[0] : issued + ((qt - q_s) >> 2)) - wt.first[0];
-        const bool in0 = st0 != 0u && (bstart + (uint32_t)lane - wt.first[0]) < len0;
+        const uint32_t cp = wt.cur;
+        const bool newer = (int32_t)(bstart + (uint32_t)lane - wt.first[cp]) >= 0;
+        const bool in0 = newer == (cp == 0u);
         if (lane < bn) {
           if (in0) S0 += o; else S1 += o;
           if (want_olt) {  // the maximum needs no canonical order
@@ -366,7 +369,9 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       }
       bn = 0;
     }
-    settle((FX && fn != 0) ? fstart : issued);  // every hit before the filter batch is consumed now
+    // one lane per row: trials are finalized lazily (at the start of the trial that reuses their parity,
+    // or at the end), not after every batch
+    if constexpr (!kCarry) settle(issued);
   };
   // Issue the next n (<= 32) queued hits as a batch (consuming the previous batch first).
   auto issue = [&](int n) {
@@ -465,9 +470,20 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     // the trial's first full window is requested before the bookkeeping below, so its latency overlaps it
     uint4 wfirst = make_uint4(0u, 0u, 0u, 0u);
     if (wf1 != 0u) wfirst = ld_ids4_stream(reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint4*>(p.ids + b) + lane));
-    if (wt.state[par] != 0u) flush();  // trial k-2 still has hits in flight
+    if (wt.state[par] != 0u) {  // trial k-2 is not finalized yet
+      // first stream position not consumed yet
+      const uint32_t done = bn != 0 ? bstart : ((FX && fn != 0) ? fstart : issued);
+      if (wt.state[par] == 2u && (int32_t)(done - wt.end[par]) >= 0) {
+        finalize(par);  // all its hits are consumed
+      } else {
+        flush();  // trial k-2 still has hits in flight
+        for (int a = 0; a < 2; ++a)
+          if (wt.state[a] == 2u) finalize(a);
+      }
+    }
     __syncwarp();
     if (lane == 0) {  // warp-uniform bookkeeping in shared memory (one writer, then a warp barrier)
+      wt.cur = (uint32_t)par;
       wt.trial[par] = t;
       wt.first[par] = issued + ((qt - q_s) >> 2);  // stream position of the trial's first hit
       wt.state[par] = 1u;
@@ -539,14 +555,10 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       wt.state[par] = 2u;
     }
     __syncwarp();
-    if (!kCarry) {
-      flush();  // wide rows: one trial at a time (finalized by the flush's settle)
-    } else if (bn == 0 && (!FX || fn == 0)) {
-      settle(issued);  // nothing pending: a trial with no outstanding hits is final now
-    }
+    if (!kCarry) flush();  // full-row batches: one trial at a time (finalized by the flush's settle)
   }
   flush();
-  // a trial with no hits after the last flush is already finalized by consume()/the check above
+  // every hit is consumed now: finalize the (at most two) trials still open
   for (int a = 0; a < 2; ++a)
     if (wt.state[a] == 2u) finalize(a);
   bad = __reduce_or_sync(FULL, bad);
