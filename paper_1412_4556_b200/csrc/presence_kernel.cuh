@@ -466,10 +466,12 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     }
     const uint32_t len = (uint32_t)(e - b);
     const bool vec = vec_ok && ((b & 3u) == 0);
-    const uint32_t wf1 = vec ? len / 128u : 0u;  // full windows
     // the trial's first full window is requested before the bookkeeping below, so its latency overlaps it
+    // aligned trial whose length is a multiple of 4: every window is whole 16-B vectors, the last one
+    // lane-masked (lanes past the end keep stale ids that their mask hides)
+    const bool valn = vec && (len & 3u) == 0u;
     uint4 wfirst = make_uint4(0u, 0u, 0u, 0u);
-    if (wf1 != 0u) wfirst = ld_ids4_stream(reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint4*>(p.ids + b) + lane));
+    if (valn && 4u * (uint32_t)lane < len) wfirst = ld_ids4_stream(p.ids + b + 4u * (uint32_t)lane);
     if (wt.state[par] != 0u) {  // trial k-2 is not finalized yet
       // first stream position not consumed yet
       const uint32_t done = bn != 0 ? bstart : ((FX && fn != 0) ? fstart : issued);
@@ -518,36 +520,32 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
       return v;
     };
     auto rel0 = [&](uint32_t w) -> uint32_t { return w * 128u + 4u * (uint32_t)lane; };
-    uint32_t w = 0;
-    if (wf1 != 0u) {  // full windows: running pointer, one window held ahead (two register sets, unrolled)
-      const uint4* lp = reinterpret_cast<const uint4*>(p.ids + b) + lane;
-      uint4 wa = wfirst, wb;
-      uint32_t rem = wf1 - 1u;  // full windows after the one in wa
-      while (true) {
-        if (rem != 0u) wb = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp + 32));
-        scan(wa, BoolC<false>{}, 0u, 0u, 0xffffffffu);
-        if (rem == 0u) break;
-        --rem;
-        lp += 64;
-        if (rem != 0u) wa = ld_ids4_stream(reinterpret_cast<const uint32_t*>(lp));
-        scan(wb, BoolC<false>{}, 0u, 0u, 0xffffffffu);
-        if (rem == 0u) break;
-        --rem;
-      }
-      w = wf1;
-    }
-    if (vec && (len & 3u) == 0u) {
-      // aligned trial whose length is a multiple of 4: the tail window is whole 16-B vectors, lanes past
-      // the end masked as a unit (no per-slot checks)
-      for (; w < nwin; ++w) {
-        const uint32_t r = rel0(w);
-        const bool ok = r < len;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (ok) v = ld_ids4_stream(p.ids + b + r);
-        scan(v, BoolC<false>{}, 0u, 0u, ok ? 0xffffffffu : 0u);
+    if (valn) {
+      // windows streamed through a running per-lane pointer, one window held ahead in registers (two
+      // register sets, unrolled); window w covers trial positions r .. r+3 of this lane, r = 128 w + 4 l
+      if (nwin != 0u) {
+        const uint32_t* lpp = p.ids + b + 4u * (uint32_t)lane;
+        uint32_t r = 4u * (uint32_t)lane;
+        uint4 wa = wfirst, wb = wfirst;
+        uint32_t rem = nwin - 1u;  // windows after the one in wa
+        bool ok_a = r < len, ok_b;
+        while (true) {
+          ok_b = r + 128u < len;
+          if (rem != 0u && ok_b) wb = ld_ids4_stream(lpp + 128);
+          scan(wa, BoolC<false>{}, 0u, 0u, ok_a ? 0xffffffffu : 0u);
+          if (rem == 0u) break;
+          --rem;
+          lpp += 256;
+          r += 256u;
+          ok_a = r < len;
+          if (rem != 0u && ok_a) wa = ld_ids4_stream(lpp);
+          scan(wb, BoolC<false>{}, 0u, 0u, ok_b ? 0xffffffffu : 0u);
+          if (rem == 0u) break;
+          --rem;
+        }
       }
     } else {
-      for (; w < nwin; ++w) scan(load_checked(w), BoolC<true>{}, rel0(w), len, 0xffffffffu);  // tail (or unaligned trial)
+      for (uint32_t w = 0; w < nwin; ++w) scan(load_checked(w), BoolC<true>{}, rel0(w), len, 0xffffffffu);  // unaligned trial
     }
     __syncwarp();
     if (lane == 0) {
