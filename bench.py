@@ -618,7 +618,7 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
                                       "launch_ms": ms, "eff_GBps": occ * (4 + rb) / ms / 1e6}), file=sys.stderr, flush=True)
     ctx.ara_set_option(ara.ARA_OPT_VARIANT, 0)
     if presence:
-        ctx.ara_set_option(ara.ARA_OPT_PREFETCH, 1)
+        ctx.ara_set_option(ara.ARA_OPT_PREFETCH, 0)  # the library default
     ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, 0)
     ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, 0)
     ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, 0)

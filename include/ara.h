@@ -199,8 +199,9 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *   ARA_OPT_L2_POLICY       0 default (evict_last hints on table rows and records; the dense kernel
  *                           also marks YET ids evict_first), 1 no hints, 2 hints + persisting
  *                           access-policy window on the table
- *   ARA_OPT_PREFETCH        presence kernel: 1 (default) each warp prefetches its next trial's ids
- *                           into L2 at the start of a trial, 0 off
+ *   ARA_OPT_PREFETCH        presence kernel: 1 each warp prefetches its next trial's ids into L2 at
+ *                           the start of a trial, 0 (default) off -- every window, the trial's first
+ *                           and last included, is already requested one step ahead in registers
  *   ARA_OPT_VARIANT         kernel variant index within the selected kernel and row width
  *                           (ara_layer_info reports the count)
  *   ARA_OPT_KERNEL          -1 auto (default): per layer, the presence kernel when its folded bitmap is

@@ -96,7 +96,7 @@ struct ara_ctx {
   int block_threads = 256;
   int blocks_per_sm = 0;
   int l2_policy = 0;
-  int prefetch = 1;
+  int prefetch = 0;  // ARA_OPT_PREFETCH (measured slower since every window is register-prefetched)
   int filter = -1;  // ARA_OPT_FILTER: -1 auto, 0 off, 1 on
   int precombined = 0;  // ARA_OPT_PRECOMBINED: 1 = gather o[e] from the precombined table
   int variant = 0;
