@@ -53,7 +53,7 @@ struct LayerParams {
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
 
-// Sparse record of one table row (built by ara_create for rows of <= 16 columns):
+// Sparse record of one table row (built by ara_create for every layer, any row width <= kMaxJ):
 //   x = c1 | c2 << 8 | n << 16   (n = non-zero losses in the row; c1 < c2 their columns, layer order)
 //   y = bits of the loss in column c1 (0 if n == 0), z = bits of the loss in column c2 (0 if n < 2)
 //   w = the event id (row index)

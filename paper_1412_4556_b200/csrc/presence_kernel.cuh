@@ -5,18 +5,22 @@
 // c9), so only rows whose bit is set are gathered.  The bitmap lives in SHARED memory (one copy per SM,
 // folded modulo its capacity when C+1 exceeds it -- folding only adds false positives, i.e. gathers of
 // rows that turn out to be zero, never misses), so the per-occurrence test costs one LDS instead of a
-// 64-B gather.  The kernel is then bound by streaming the YET ids from HBM.
+// 64-B gather.  The kernel is then bound by instruction issue (P) or by the record gathers (X).
 //
 //   * one warp per trial (persistent grid); the warp streams the trial's ids in 128-id windows, each lane
-//     one 16-B vector (L1::no_allocate, L2 evict_first), with the next window prefetched;
-//   * per window slot: validity check, bitmap test, __ballot_sync; hits (event ids) are appended to a
-//     per-warp ring queue in shared memory (64 entries);
-//   * whenever 32 hits are queued the warp drains them with all lanes active: each queued event's row is
-//     gathered by G lanes (V-float vectors, 256-bit loads), FT1 is applied in fp64 to its non-zero
-//     entries and summed, the G partials are combined, FT2 is applied and the leader lane accumulates
-//     the occurrence-net loss (steps 1-4);
-//   * at the end of the trial the remaining hits are drained, the lanes' sums are reduced with shuffles
-//     and FT3 is applied to S_n.
+//     one 16-B vector (L1::no_allocate), one window requested ahead in registers; the trial's first window
+//     is requested before the per-trial bookkeeping and its last (partial) window is lane-masked inside
+//     the same loop, so no load sits on the critical path;
+//   * per window: bitmap test per id (the folded word's bit, a sentinel bit for invalid ids), one ballot
+//     per pair of slots appends the hits to a linear per-warp queue in shared memory;
+//   * whenever 32 hits are queued the warp consumes the previous batch and issues the next: with one lane
+//     per row (G == 1, the default for every width) each lane cp.asyncs its event's 16-B sparse record
+//     (first two non-zero columns; rows with more are read in full), applies FT1 in fp64 to those losses,
+//     sums them, applies FT2 and accumulates the occurrence-net loss of the trial that owns the hit
+//     (steps 1-3); G > 1 variants gather full rows round by round;
+//   * the queue is carried across the warp's trials; a trial is finalized lazily -- when the trial that
+//     reuses its parity slot starts, or at the end -- by a fixed rotation + xor-tree of the lanes' sums,
+//     then FT3 on S_n (step 4) and one 8-B YLT store.
 #pragma once
 #include "ara_kernel.cuh"
 
@@ -126,7 +130,7 @@ struct RowBatch {
   }
 };
 
-// Narrow rows (<= 16 columns, one lane per row): the batch holds each queued event's 16-byte sparse
+// One lane per row (G == 1, any row width): the batch holds each queued event's 16-byte sparse
 // RECORD instead of its full row.  Typically a present row has a single non-zero loss (the ELTs are
 // sparse and nearly disjoint), so steps 1-3 cost two FT1 clamps and one FT2 clamp per row; a row with
 // more than two losses (rare) is read in full from the table.  The sum runs over the non-zero columns
@@ -235,7 +239,7 @@ struct BoolC {
 // SENTINEL bit is always set, so invalid ids are queued like hits and reported when their batch is
 // issued: the scan itself needs no validity check.
 //
-// Hits are queued as raw event ids and, for narrow rows (G == 1), the queue is CARRIED across the warp's
+// Hits are queued as raw event ids and, with one lane per row (G == 1), the queue is CARRIED across the warp's
 // consecutive trials: batches are always full (32 rows) except when the queue must be flushed, so the
 // per-trial partial batch disappears.  A queued hit's trial follows from its stream position (each open
 // trial owns [first, end)).  The occurrence-net loss of the i-th hit of a trial is always accumulated by
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   // branch-free FT1 of a padding column -- always loss 0 -- is exactly +0).
   constexpr int JPS = G * ((NV + G - 1) / G) * V;
   __shared__ double s_r1[JPS], s_l1[JPS];
-  __shared__ double2 s_t1[kCarry ? JPS : 1];  // narrow rows: FT1 as (R, L) pairs, one 16-B load per column
+  __shared__ double2 s_t1[kCarry ? JPS : 1];  // record batches: FT1 as (R, L) pairs, one 16-B load per column
   __shared__ WarpTrials s_wt[NW];
   uint32_t* bits = smem;  // [present_words], already folded by the host (fold_mul)
   const int warp = threadIdx.x >> 5;
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   uint32_t* q = smem + p.present_words + warp * kQueue;
   WarpTrials& wt = s_wt[warp];
   const uint32_t q_s = (uint32_t)__cvta_generic_to_shared(q);  // 32-bit shared addresses
-  // record slots (narrow rows): 32 x 16 B per warp after the queues, 16-B aligned
+  // record slots (G == 1): 32 x 16 B per warp after the queues, 16-B aligned
   const uint32_t rec_s = (((uint32_t)__cvta_generic_to_shared(smem + p.present_words + NW * kQueue) + 15u) & ~15u) +
                          (uint32_t)warp * 512u;
 
