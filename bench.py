@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--l2-policy", type=int, default=None)
     ap.add_argument("--filter", type=int, default=None, choices=[-1, 0, 1],
                     help="ARA_OPT_FILTER: exact filter stage of the record presence kernel (-1 auto)")
+    ap.add_argument("--stream", type=int, default=None,
+                    help="ARA_OPT_STREAM: 0 = presence kernel for fixed-length trials, 1..3 = stream kernel variant")
+    ap.add_argument("--prefetch", type=int, default=None, choices=[-1, 0, 1], help="ARA_OPT_PREFETCH")
+    ap.add_argument("--round-min", type=int, default=None, help="ARA_OPT_ROUND_MIN (lane kernel round trigger)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cold", action="store_true")
@@ -156,6 +160,21 @@ class ClockSampler:
                 "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+def host_cpu():
+    """lscpu model and topology of the host running the oracle."""
+    info = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            info[k.strip()] = v.strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return {"model": info.get("Model name"), "sockets": info.get("Socket(s)"),
+            "cores_per_socket": info.get("Core(s) per socket"), "threads_per_core": info.get("Thread(s) per core"),
+            "online_cpus": info.get("On-line CPU(s) list"), "affinity_cpus": len(os.sched_getaffinity(0))}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -199,7 +218,8 @@ def run_reference(args):
                    "events_per_trial": [cfg.kmin, cfg.kmax], "layers": len(cfg.layers),
                    "elts_per_layer": len(cfg.layers[0].elts), "catalog": cfg.catalog_size,
                    "parallelism": f"oracle threads={cores}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "host": host_cpu(),
+                         "extrapolation": cfg.num_trials / sample,
                          "sample": f"{sample} evenly spaced trials per step of {cfg.num_trials}; value extrapolated "
                                    f"x{cfg.num_trials / sample:g} to the full run"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -257,6 +277,12 @@ def main():
         ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, args.l2_policy)
     if args.filter is not None:
         ctx.ara_set_option(ara.ARA_OPT_FILTER, args.filter)
+    if args.stream is not None:
+        ctx.ara_set_option(ara.ARA_OPT_STREAM, args.stream)
+    if args.prefetch is not None:
+        ctx.ara_set_option(ara.ARA_OPT_PREFETCH, args.prefetch)
+    if args.round_min is not None:
+        ctx.ara_set_option(ara.ARA_OPT_ROUND_MIN, args.round_min)
     info = [ctx.ara_layer_info(l) for l in range(L)]
 
     # ---- this rank's YET shard, generated in HBM
@@ -322,16 +348,22 @@ def main():
         cpu_s = time.perf_counter() - c0
         got = ylt_local[:, torch.from_numpy(trials - t0).to(dev)].cpu().numpy()
         tol = np.maximum(1e-6 * np.abs(y_or), 1e-3)
-        bad = int(np.sum(np.abs(got - y_or) > tol))
+        err = np.abs(got - y_or)
+        bad = int(np.sum(err > tol))
+        nz = np.abs(y_or) > 0
+        parity = {"sampled_trials": int(sample), "max_abs_err": float(err.max()) if err.size else 0.0,
+                  "max_rel_err": float((err[nz] / np.abs(y_or[nz])).max()) if np.any(nz) else 0.0,
+                  "bitwise_equal": int(np.sum(got == y_or)), "tolerance": "|gpu - oracle| <= max(1e-6 |oracle|, 1e-3)"}
         if bad:
             print(json.dumps({"error": f"parity gate failed: {bad} of {got.size} sampled YLT values outside "
                                        f"1e-6 rel / 1e-3 abs of the oracle"}), flush=True)
             sys.exit(3)
         cpu = {"value": cpu_s * 1e3 * 1e6 / sample, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "host": host_cpu(), "extrapolation": 1e6 / sample,
                "sample": f"{sample} evenly spaced trials of rank {rank}'s shard (YLT + PML/TVaR on the sample), "
                          f"{cpu_s:.2f} s wall; value extrapolated to 1M trials; the same sample gates GPU parity "
                          f"(0 of {got.size} outside tolerance)",
-               "parity_checked": int(got.size)}
+               "parity_checked": int(got.size), "parity": parity}
 
     clk = ClockSampler(dev.index).start()  # started before the warm-up: no tool start-up inside the timed region
     for _ in range(args.warmup):
@@ -434,14 +466,16 @@ def main():
     row_bytes = [max(32, i["row_stride"]) for i in info]  # sector-rounded row bytes
     launch_ms = kern_ms / L
     peak, peak_src = peaks()
-    kernel_name = info[0]["variant"].split("<")[0]
+    kernel_full = ctx.ara_kernel_name()  # the kernel the timed runs launched
+    kernel_name = kernel_full.split("<")[0]
+    sparse_path = kernel_name in ("ara_presence_kernel", "ara_stream_kernel")
     # compulsory HBM bytes of one presence-kernel launch: the YET ids (4 B per occurrence), the YLT
     # row (8 B per trial), and one read of every table row that holds a loss plus the bitmap
     present_rows = [ctx.ara_layer_stats(l)["present_rows"] for l in range(L)]
     comp_bytes = float(np.mean([4.0 * occ + 8.0 * n_local + pr * rb + (cfg.catalog_size + 1) / 8.0
                                 for pr, rb in zip(present_rows, row_bytes)]))
     dense_bytes = float(np.mean([occ * (4 + rb) for rb in row_bytes]))  # 4 B id + row sectors
-    if kernel_name == "ara_presence_kernel":
+    if sparse_path:
         alg_bytes_launch = comp_bytes
         alg_note = ("algorithmic bytes = compulsory HBM traffic: 4 B YET id per occurrence + 8 B YLT per trial + "
                     "one read of each table row holding a loss (%d rows x %d B) + the presence bitmap; rows of "
@@ -456,12 +490,13 @@ def main():
     if os.path.exists(prof):
         with open(prof) as f:
             pj = json.load(f)
-        if pj.get("variant") == info[0]["variant"] and world == 1:  # the capture is of the N = 1 launch
+        if pj.get("variant") == kernel_full and world == 1:  # the capture is of the N = 1 launch
             traffic = pj.get("dram_bytes_per_launch")
 
     # ---- the dense direct-access kernel (every occurrence gathers its full row), timed beside
     dense = None
-    if not args.profile and args.variant is None and kernel_name == "ara_presence_kernel":
+    presence_leg = None
+    if not args.profile and args.variant is None and sparse_path:
         ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_DENSE)
         for _ in range(2):
             ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
@@ -483,9 +518,23 @@ def main():
     # ---- SURVEY N3 ablation: the precombined occurrence-net table o[e] (no ELT lookups at run time),
     # timed beside; its YLT must equal the product path's bit for bit (checked here)
     pre = None
-    if not args.profile and args.variant is None and kernel_name == "ara_presence_kernel":
+    if not args.profile and args.variant is None and sparse_path:
         ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
         ref_ylt = ylt_local.clone()  # the product path's YLT
+        # the round-1 presence kernel (stream kernel off), timed beside: its YLT must equal bit for bit
+        if kernel_name == "ara_stream_kernel":
+            ctx.ara_set_option(ara.ARA_OPT_STREAM, 0)
+            for _ in range(2):
+                ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(5):
+                ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            presence_leg = {"kernel": ctx.ara_kernel_name(), "launch_ms": a.elapsed_time(b) / 5 / L,
+                            "ylt_bitwise_equal": bool(torch.equal(ylt_local, ref_ylt))}
+            ctx.ara_set_option(ara.ARA_OPT_STREAM, 1 if args.stream is None else args.stream)
         ctx.ara_set_option(ara.ARA_OPT_PRECOMBINED, 1)
         for _ in range(2):
             ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
@@ -522,7 +571,7 @@ def main():
                        if world > 1 else ""),
                    "l2": "no flush: inputs (YET %.1f GB) exceed L2; table L2-resident by design (cold_l2_ms beside)"
                          % (n_ids * 4 / 1e9),
-                   "kernel": info[0]["variant"], "storage": "fp32 ELT losses, fp64 terms/sums/YLT"},
+                   "kernel": kernel_full, "storage": "fp32 ELT losses, fp64 terms/sums/YLT"},
         "trials_per_s": N / (ms_per_step * 1e-3),
         "elt_lookups_per_s": lookups_exact / (ms_per_step * 1e-3),
         "kernel_ms_per_step": kern_ms, "create_ms": create_ms, "cold_l2_ms_per_step": cold_ms,
@@ -532,6 +581,7 @@ def main():
                      "effective_GBps_68B": dense_bytes / (launch_ms * 1e-3) / 1e9,
                      "note": alg_note + f"; peak {peak_src}"},
         "dense_kernel": dense,
+        "presence_kernel": presence_leg,
         "precombined_N3": pre,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -541,6 +591,7 @@ def main():
     print(json.dumps(line), flush=True)
 
     if args.sweep:
+        info[0]["product_kernel"] = kernel_full
         sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ)
     if args.study:
         study(ctx, cfg, ids, offsets_d, offsets_h, K, n_local, L, ylt_local, stream, occ, kern_ms)
@@ -586,8 +637,29 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
     import torch
 
     from paper_1412_4556_b200 import ara
-    nv = info[0]["num_variants"]
     rb = max(32, info[0]["row_stride"])
+    if info[0].get("product_kernel", "").startswith(("ara_stream", "ara_lane")):  # fixed-length-trial kernels
+        for sv in (1, 2, 3, 4):
+            for pf in (0, 1):
+                for pol in (0, 1):
+                    ctx.ara_set_option(ara.ARA_OPT_STREAM, sv)
+                    ctx.ara_set_option(ara.ARA_OPT_PREFETCH, pf)
+                    ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, pol)
+                    for _ in range(2):
+                        ctx.ara_run(ids, ylt_local, offsets=None, events_per_trial=K, num_trials=n_local, stream=stream)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    for _ in range(5):
+                        ctx.ara_run(ids, ylt_local, offsets=None, events_per_trial=K, num_trials=n_local, stream=stream)
+                    b.record(stream)
+                    torch.cuda.synchronize()
+                    print(json.dumps({"sweep": ctx.ara_kernel_name(), "prefetch": pf, "l2_policy": pol,
+                                      "launch_ms": a.elapsed_time(b) / 5 / L}), file=sys.stderr, flush=True)
+        ctx.ara_set_option(ara.ARA_OPT_STREAM, 1)
+        ctx.ara_set_option(ara.ARA_OPT_PREFETCH, 0)
+        ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, 0)
+        ctx.ara_set_option(ara.ARA_OPT_STREAM, 0)  # then the presence kernel's own sweep
+    nv = info[0]["num_variants"]
     presence = info[0]["variant"].startswith("ara_presence")
     for v in range(nv):
         # presence kernels fix their block size: sweep the next-trial prefetch instead of block threads
@@ -622,6 +694,7 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
     ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, 0)
     ctx.ara_set_option(ara.ARA_OPT_BLOCKS_PER_SM, 0)
     ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, 0)
+    ctx.ara_set_option(ara.ARA_OPT_STREAM, 1)
 
 
 if __name__ == "__main__":

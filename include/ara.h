@@ -225,6 +225,12 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           with the option set) instead of the sparse records.  Bitwise identical
  *                           YLT; exact only for deterministic losses (no secondary uncertainty,
  *                           PAPER.md:125), and no ELT lookups happen at run time.
+ *   ARA_OPT_STREAM          1 (default): for a YET of fixed-length trials (no offsets, K % 4 == 0, 16-B
+ *                           aligned ids) the presence path runs the stream kernel (stream_kernel.cuh:
+ *                           contiguous trial blocks per warp, a register-held trial ring, fewer
+ *                           instructions per occurrence); v = 1..3 selects its variant (32, 24, 16 warps
+ *                           per block); 0 = always the presence kernel.  Bitwise identical YLT (the same
+ *                           per-trial summation order).
  * ARA_OPT_BLOCK_THREADS applies to the dense kernel; the presence kernel fixes its block size. */
 typedef enum {
   ARA_OPT_BLOCK_THREADS = 1,
@@ -234,7 +240,9 @@ typedef enum {
   ARA_OPT_KERNEL = 5,
   ARA_OPT_PREFETCH = 6,
   ARA_OPT_FILTER = 7,
-  ARA_OPT_PRECOMBINED = 8
+  ARA_OPT_PRECOMBINED = 8,
+  ARA_OPT_STREAM = 9,
+  ARA_OPT_ROUND_MIN = 10
 } ara_option;
 ARA_API ara_status ara_set_option(ara_ctx* ctx, ara_option opt, int64_t value);
 ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);
@@ -250,6 +258,10 @@ ARA_API ara_status ara_layer_info(ara_ctx* ctx, uint32_t layer, uint64_t* table_
  * ARA_OPT_KERNEL (0 presence, 1 dense).  Any output pointer may be NULL. */
 ARA_API ara_status ara_layer_stats(ara_ctx* ctx, uint32_t layer, uint64_t* present_rows, double* est_hit_rate,
                                    int* kernel);
+
+/* Name of the kernel the most recent ara_run / ara_run_ex / ara_run_host of this context launched for
+ * its last layer (a static string; "" before the first run). */
+ARA_API const char* ara_kernel_name(ara_ctx* ctx);
 
 /* Test hook: copy row `event` of layer l's table (row_stride bytes) to HOST out.  Synchronous. */
 ARA_API ara_status ara_table_row(ara_ctx* ctx, uint32_t layer, uint32_t event, float* out);

@@ -19,11 +19,11 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-I", INCLUDE, "-Xptxas", "-warn-spills"]
 
 LIBS = {
-    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_api.cu", "metrics.cu", "kernels_presence.cu", "kernels_presence_mid.cu", "kernels_presence_wide.cu", "kernels_dense.cu", "kernels_study.cu", "outputs.cu")],
+    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_api.cu", "metrics.cu", "kernels_presence.cu", "kernels_presence_mid.cu", "kernels_presence_wide.cu", "kernels_dense.cu", "kernels_study.cu", "outputs.cu", "kernels_stream.cu")],
     "libara_synth.so": [os.path.join(HERE, "synth", "synth.cu")],
 }
 DEPS = {
-    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_kernel.cuh", "presence_kernel.cuh", "variants.cuh", "study.cuh", "common.cuh")] + [os.path.join(INCLUDE, "ara.h")],
+    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_kernel.cuh", "presence_kernel.cuh", "stream_kernel.cuh", "lane_kernel.cuh", "variants.cuh", "study.cuh", "common.cuh")] + [os.path.join(INCLUDE, "ara.h")],
     "libara_synth.so": [os.path.join(INCLUDE, "ara_synth.h")],
 }
 OUT_DIR = {"libara.so": HERE, "libara_synth.so": os.path.join(HERE, "synth")}

@@ -25,6 +25,8 @@ ARA_OPT_BLOCK_THREADS, ARA_OPT_BLOCKS_PER_SM, ARA_OPT_L2_POLICY, ARA_OPT_VARIANT
 ARA_OPT_PREFETCH = 6
 ARA_OPT_FILTER = 7
 ARA_OPT_PRECOMBINED = 8
+ARA_OPT_STREAM = 9
+ARA_OPT_ROUND_MIN = 10
 KERNEL_AUTO, KERNEL_PRESENCE, KERNEL_DENSE = -1, 0, 1
 STUDY_INTERLEAVED, STUDY_INDEPENDENT, STUDY_SORTED = 0, 1, 2
 ARA_MAX_ELTS_PER_LAYER = 128
@@ -33,7 +35,8 @@ ARA_MAX_ELTS_PER_LAYER = 128
 EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_ex", "ara_run_host", "ara_run_study", "ara_aal", "ara_ep",
            "ara_sum_layers", "ara_check", "ara_pml_tvar", "ara_pml",
            "ara_tvar", "ara_pml_tvar_device", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
-           "ara_layer_info", "ara_layer_stats", "ara_table_row", "ara_status_string", "ara_last_error", "ara_version")
+           "ara_layer_info", "ara_layer_stats", "ara_table_row", "ara_kernel_name", "ara_status_string", "ara_last_error",
+           "ara_version")
 
 
 class AraError(RuntimeError):
@@ -97,6 +100,7 @@ def lib() -> ctypes.CDLL:
             "ara_layer_stats": (st, [vp, u32, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_int)]),
             "ara_table_row": (st, [vp, u32, u32, dp]),
+            "ara_kernel_name": (ctypes.c_char_p, [vp]),
             "ara_status_string": (ctypes.c_char_p, [ctypes.c_int]),
             "ara_last_error": (ctypes.c_char_p, []),
             "ara_version": (u32, []),
@@ -277,6 +281,10 @@ class Context:
         _check(lib().ara_layer_stats(self._h, layer, ctypes.byref(pr), ctypes.byref(hr), ctypes.byref(k)),
                "ara_layer_stats")
         return {"present_rows": pr.value, "est_hit_rate": hr.value, "kernel": k.value}
+
+    def ara_kernel_name(self) -> str:
+        """Kernel the last run launched (for reports)."""
+        return lib().ara_kernel_name(self._h).decode()
 
     def ara_table_row(self, layer: int, event: int) -> np.ndarray:
         stride = self.ara_layer_info(layer)["row_stride"]

@@ -15,6 +15,8 @@
 #include "ara.h"
 #include "ara_kernel.cuh"
 #include "presence_kernel.cuh"
+#include "stream_kernel.cuh"
+#include "lane_kernel.cuh"
 #include "variants.cuh"
 #include "study.cuh"
 #include "common.cuh"
@@ -64,10 +66,15 @@ struct Layer {
   float* table = nullptr;
   uint64_t table_bytes = 0;
   uint32_t* present = nullptr;  // presence bitmap, (C + 1 + 31) / 32 words: bit e set iff row e holds a loss
-  uint32_t* folded = nullptr;   // the bitmap folded for the presence kernel's shared memory (same size)
-  uint32_t folded_words = 0;    // words of the current fold (0: not built yet)
-  uint32_t fold_mul = 0;        // its multiplier (LayerParams::fold_mul)
-  uint4* rec = nullptr;         // sparse row records (C + 1) x 16 B (presence kernels with one lane per row)
+  // the bitmap folded into the words a kernel's shared memory holds, one buffer per fold size (never
+  // rebuilt in place, so a launch still reading one fold cannot see another being built)
+  struct Fold {
+    uint32_t words, mul;
+    uint32_t* buf;
+  };
+  std::vector<Fold> folds;
+  uint32_t fold_words = 0;  // canonical fold size of this layer (every presence/stream launch uses it)
+  uint4* rec = nullptr;         // sparse row records (C + 2) x 16 B; record C + 1 is all zero (invalid ids)
   double* occ = nullptr;        // precombined o[e] per event, (C + 1) x 8 B, built on first use
   // Section IV.B study structures, built on first use by ara_run_study
   float* indep = nullptr;         // J x (C + 1) independent per-ELT direct-access arrays
@@ -87,6 +94,13 @@ struct Layer {
 
 struct ara_ctx {
   int device = 0;
+  // per-kernel static shared memory and the largest dynamic size already set (host-side launch cache)
+  struct FnInfo {
+    const void* fn;
+    int static_smem;
+    int dyn_set;
+  };
+  std::vector<FnInfo> fn_info;
   int sms = 148;
   uint32_t C = 0;
   std::vector<ara::Layer> layers;
@@ -96,11 +110,14 @@ struct ara_ctx {
   int block_threads = 256;
   int blocks_per_sm = 0;
   int l2_policy = 0;
-  int prefetch = 0;  // ARA_OPT_PREFETCH (measured slower since every window is register-prefetched)
+  int prefetch = -1;  // ARA_OPT_PREFETCH: -1 auto (stream kernel: on; presence kernel: off), 0 off, 1 on
   int filter = -1;  // ARA_OPT_FILTER: -1 auto, 0 off, 1 on
   int precombined = 0;  // ARA_OPT_PRECOMBINED: 1 = gather o[e] from the precombined table
   int variant = 0;
   int kernel = -1;  // KernelKind, or -1 = per-layer automatic choice
+  int round_min = 24;     // ARA_OPT_ROUND_MIN: lane kernel round trigger (lanes holding a queued hit)
+  int stream_kernel = 1;  // ARA_OPT_STREAM: 0 off, v > 0 = stream variant v - 1 for fixed-length trials
+  const char* last_kernel = "";  // name of the kernel the last launch used (layer 0)
   int persist_max = 0, window_max = 0;
   int smem_optin = 0;
   // end-to-end host path
@@ -248,7 +265,7 @@ static void destroy_ctx(ara_ctx* c) {
   for (auto& L : c->layers) {
     cudaFree(L.table);
     cudaFree(L.present);
-    cudaFree(L.folded);
+    for (auto& f : L.folds) cudaFree(f.buf);
     cudaFree(L.rec);
     cudaFree(L.occ);
     cudaFree(L.indep);
@@ -286,6 +303,76 @@ static const Variant* pick(const ara_ctx* c, const Layer& L) {
   return vs[v];
 }
 
+// Static shared memory of a kernel, cached per context (cudaFuncGetAttributes once per kernel).
+static ara_status fn_static_smem(ara_ctx* c, const void* fn, int* out) {
+  for (auto& f : c->fn_info)
+    if (f.fn == fn) {
+      *out = f.static_smem;
+      return ARA_OK;
+    }
+  cudaFuncAttributes fa;
+  ARA_CUDA(cudaFuncGetAttributes(&fa, fn));
+  c->fn_info.push_back({fn, (int)fa.sharedSizeBytes, 0});
+  *out = (int)fa.sharedSizeBytes;
+  return ARA_OK;
+}
+
+// Raise a kernel's dynamic shared-memory limit only when a launch needs more than already set.
+static ara_status fn_dyn_smem(ara_ctx* c, const void* fn, size_t bytes) {
+  int dummy;
+  ara_status st = fn_static_smem(c, fn, &dummy);
+  if (st) return st;
+  for (auto& f : c->fn_info)
+    if (f.fn == fn) {
+      if ((int)bytes > f.dyn_set) {
+        ARA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        f.dyn_set = (int)bytes;
+      }
+      return ARA_OK;
+    }
+  return ARA_OK;
+}
+
+// The layer's presence bitmap folded into `words` words (built on first use, stream-ordered; one buffer
+// per fold size, so a fold is never rebuilt while an earlier launch may still read it).
+static ara_status get_fold(ara_ctx* c, Layer& L, uint32_t words, cudaStream_t stream, const uint32_t** buf,
+                           uint32_t* mul_out) {
+  const uint64_t C = c->C;
+  const uint32_t fw = (uint32_t)std::min<uint64_t>(L.present_words, words);
+  const uint32_t mul = (C + 1 <= 32ull * fw) ? (1u << 27) : (uint32_t)((((uint64_t)fw << 32) - 1) / C);
+  for (auto& f : L.folds)
+    if (f.words == fw && f.mul == mul) {
+      *buf = f.buf;
+      *mul_out = mul;
+      return ARA_OK;
+    }
+  uint32_t* b = nullptr;
+  if (cudaMalloc(&b, (size_t)fw * 4) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ARA_E_NOMEM, "folded presence bitmap");
+  }
+  ARA_CUDA(cudaMemsetAsync(b, 0, (size_t)fw * 4, stream));
+  const unsigned fb = (unsigned)std::min<uint64_t>((L.present_words + 255) / 256, 4096);
+  presence_fold_kernel<<<fb, 256, 0, stream>>>(b, L.present, L.present_words, c->C, mul);
+  ARA_CUDA(cudaGetLastError());
+  L.folds.push_back({fw, mul, b});
+  *buf = b;
+  *mul_out = mul;
+  return ARA_OK;
+}
+
+// The fixed-length-trial kernel applies to a YET of fixed length K (K % 4 == 0, 16-B aligned ids), a
+// catalogue below 2^32 - 2 and per-warp hit ordinals that cannot wrap.
+static bool stream_eligible(const ara_ctx* c, const uint32_t* ids, const uint64_t* offsets, uint64_t num_trials,
+                            uint32_t K, int nw) {
+  if (c->stream_kernel <= 0 || offsets || K == 0 || (K & 3u) || (reinterpret_cast<uintptr_t>(ids) & 15u)) return false;
+  if (c->filter == 1 || c->precombined) return false;  // those ablations live in the presence kernel
+  if ((uint64_t)c->C + 2 > 0xffffffffull) return false;
+  const uint64_t warps = (uint64_t)c->sms * nw;
+  const uint64_t per_warp = (num_trials + warps - 1) / warps + 1;
+  return per_warp * ((K + 127ull) / 128 * 128) < (1ull << 30);
+}
+
 static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const uint64_t* offsets,
                                uint64_t num_trials, uint64_t num_events, uint32_t K, double* ylt, double* olt,
                                cudaStream_t stream) {
@@ -302,7 +389,7 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   p.C = c->C;
   p.jpad = L.jpad;
   p.l2_hints = c->l2_policy == 1 ? 0u : 1u;
-  p.prefetch = c->prefetch ? 1u : 0u;
+  p.prefetch = c->prefetch > 0 ? 1u : 0u;
   p.ylt = ylt;
   p.olt = olt;
   p.err = c->d_err;
@@ -317,25 +404,51 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   int threads = c->block_threads;
   size_t dyn_smem = 0;
   KernelFn fn = olt ? var->fn_olt : var->fn;
-  if (var->kind == KIND_PRESENCE) {
-    threads = var->NW * 32;
-    cudaFuncAttributes fa;
-    ARA_CUDA(cudaFuncGetAttributes(&fa, (const void*)var->fn));
-    const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)presence_warp_smem(var);
+  const char* name = var->name;
+  int bps = c->blocks_per_sm;
+  int nsv = 0;
+  const StreamVariant* sv = stream_variants(&nsv);
+  const StreamVariant* svar = (c->stream_kernel > 0 && c->stream_kernel <= nsv) ? &sv[c->stream_kernel - 1] : nullptr;
+  if (var->kind == KIND_PRESENCE && svar && stream_eligible(c, ids, offsets, num_trials, K, svar->NW)) {
+    // fixed-length trials: the stream kernel (stream_kernel.cuh), one block of NW warps per SM
+    fn = olt ? svar->fn_olt : svar->fn;
+    name = svar->name;
+    p.prefetch = c->prefetch != 0 ? 1u : 0u;  // auto: bulk L2 prefetch two trials ahead
+    threads = svar->NW * 32;
+    int st_smem = 0;
+    ara_status st = fn_static_smem(c, (const void*)fn, &st_smem);
+    if (st) return st;
+    const uint32_t extra = svar->ring ? stream_smem_extra(L.jpad, svar->NW) : lane_smem_extra(L.jpad, svar->NW);
+    const int64_t budget = (int64_t)c->smem_optin - st_smem - (int64_t)extra;
     if (budget < 4096) return set_error(ARA_E_UNSUPPORTED, "no shared memory left for the presence bitmap");
-    // fold the bitmap into the words that fit (rebuilt, stream-ordered, when the budget changes)
-    const uint32_t fw = (uint32_t)std::min<int64_t>(L.present_words, budget / 4);
+    const uint32_t* fold = nullptr;
+    uint32_t mul = 0;
+    const uint32_t fw = (uint32_t)std::min<int64_t>(L.fold_words, budget / 4);
+    st = get_fold(c, L, fw, stream, &fold, &mul);
+    if (st) return st;
+    p.present = fold;
+    p.rec = L.rec;
+    p.present_words = fw;
+    p.fold_mul = mul;
+    dyn_smem = (size_t)fw * 4 + extra;
+    p.round_min = (uint32_t)c->round_min;
+    st = fn_dyn_smem(c, (const void*)fn, dyn_smem);
+    if (st) return st;
+    bps = 1;
+  } else if (var->kind == KIND_PRESENCE) {
+    threads = var->NW * 32;
+    int st_smem = 0;
+    ara_status st = fn_static_smem(c, (const void*)var->fn, &st_smem);
+    if (st) return st;
+    const int64_t budget = (int64_t)c->smem_optin - st_smem - (int64_t)presence_warp_smem(var);
+    if (budget < 4096) return set_error(ARA_E_UNSUPPORTED, "no shared memory left for the presence bitmap");
+    const uint32_t fw = (uint32_t)std::min<int64_t>(L.fold_words, budget / 4);
+    const uint32_t* fold = nullptr;
+    uint32_t mul = 0;
+    st = get_fold(c, L, fw, stream, &fold, &mul);
+    if (st) return st;
     const uint64_t C = c->C;
-    const uint32_t mul = (C + 1 <= 32ull * fw) ? (1u << 27) : (uint32_t)((((uint64_t)fw << 32) - 1) / C);
-    if (L.folded_words != fw || L.fold_mul != mul) {
-      ARA_CUDA(cudaMemsetAsync(L.folded, 0, (size_t)fw * 4, stream));
-      const unsigned fb = (unsigned)std::min<uint64_t>((L.present_words + 255) / 256, 4096);
-      presence_fold_kernel<<<fb, 256, 0, stream>>>(L.folded, L.present, L.present_words, c->C, mul);
-      ARA_CUDA(cudaGetLastError());
-      L.folded_words = fw;
-      L.fold_mul = mul;
-    }
-    p.present = L.folded;
+    p.present = fold;
     p.rec = L.rec;
     p.exact = L.present;
     p.present_words = fw;
@@ -359,9 +472,10 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
       p.occ = L.occ;
       fn = olt ? var->fn_pc_olt : var->fn_pc;
     }
-    ARA_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem));
+    st = fn_dyn_smem(c, (const void*)fn, dyn_smem);
+    if (st) return st;
+    if (bps <= 0) bps = 1;  // __launch_bounds__(NW * 32, 1) and a shared-memory-sized bitmap: one block per SM
   }
-  int bps = c->blocks_per_sm;
   if (bps <= 0) {
     ARA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (const void*)var->fn, threads, dyn_smem));
     if (bps < 1) bps = 1;
@@ -370,6 +484,7 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   uint64_t blocks = (uint64_t)c->sms * bps;
   uint64_t need = (num_trials + warps_per_block - 1) / warps_per_block;
   if (blocks > need) blocks = need;
+  c->last_kernel = name;
 
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof cfg);
@@ -515,8 +630,7 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
     }
     CK(cudaMemsetAsync(L.table, 0, L.table_bytes, s));
     L.present_words = (uint32_t)(((uint64_t)catalog_size + 1 + 31) / 32);
-    if (cudaMalloc(&L.present, (size_t)L.present_words * 4) != cudaSuccess ||
-        cudaMalloc(&L.folded, (size_t)L.present_words * 4) != cudaSuccess) {
+    if (cudaMalloc(&L.present, (size_t)L.present_words * 4) != cudaSuccess) {
       cudaGetLastError();
       FAIL(set_error(ARA_E_NOMEM, "presence bitmap for layer %u", l));
     }
@@ -540,7 +654,18 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       CK(cudaFuncGetAttributes(&fa, (const void*)pv->fn));
       const int64_t budget = (int64_t)c->smem_optin - (int64_t)fa.sharedSizeBytes - (int64_t)presence_warp_smem(pv);
       const double pw = (double)(((uint64_t)catalog_size + 1 + 31) / 32);
-      const double fw = budget > 0 ? std::min(pw, (double)(budget / 4)) : 1.0;
+      // canonical fold: the words the tightest kernel (the default stream variant) can hold, so every
+      // kernel tests the same candidates and sums a trial's hits in the same order (bitwise equal YLTs)
+      {
+        int nsv = 0;
+        const StreamVariant* sv = stream_variants(&nsv);
+        int64_t b = budget;
+        for (int v = 0; v < nsv; ++v)
+          b = std::min<int64_t>(b, (int64_t)c->smem_optin - (int64_t)(sv[v].ring ? stream_smem_extra(L.jpad, sv[v].NW)
+                                                                                  : lane_smem_extra(L.jpad, sv[v].NW)));
+        L.fold_words = (uint32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)pw, b / 4));
+      }
+      const double fw = budget > 0 ? std::min(pw, (double)L.fold_words) : 1.0;
       const double dens = (double)L.present_rows / ((double)catalog_size + 1.0);
       L.est_hit_rate = 1.0 - pow(1.0 - dens, std::max(1.0, pw / fw));
       // The presence kernel pays off while it skips most rows.  With one lane per row (G = 1) a hit
@@ -581,11 +706,12 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
       d_loss = nullptr;
     }
     {  // sparse row records for the one-lane-per-row presence kernels (every row width <= kMaxJ)
-      if (cudaMalloc(&L.rec, ((uint64_t)catalog_size + 1) * sizeof(uint4)) != cudaSuccess) {
+      if (cudaMalloc(&L.rec, ((uint64_t)catalog_size + 2) * sizeof(uint4)) != cudaSuccess) {
         cudaGetLastError();
         FAIL(set_error(ARA_E_NOMEM, "row records for layer %u", l));
       }
       const uint64_t rows = (uint64_t)catalog_size + 1;
+      CK(cudaMemsetAsync(L.rec + rows, 0, sizeof(uint4), s));  // record C + 1: all zero (invalid ids)
       const uint64_t rb = std::min<uint64_t>((rows + 255) / 256, (uint64_t)c->sms * 16);
       record_build_kernel<<<(unsigned)rb, 256, 0, s>>>(L.rec, L.table, L.jpad, rows);
       CK(cudaGetLastError());
@@ -846,7 +972,7 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
       c->variant = 0;
       return ARA_OK;
     case ARA_OPT_PREFETCH:
-      if (v < 0 || v > 1) return set_error(ARA_E_ARG, "prefetch in {0, 1}");
+      if (v < -1 || v > 1) return set_error(ARA_E_ARG, "prefetch in {-1, 0, 1}");
       c->prefetch = (int)v;
       return ARA_OK;
     case ARA_OPT_FILTER:
@@ -857,6 +983,18 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
       if (v < 0 || v > 1) return set_error(ARA_E_ARG, "precombined in {0, 1}");
       c->precombined = (int)v;
       return ARA_OK;
+    case ARA_OPT_ROUND_MIN:
+      if (v == 0) v = 24;
+      if (v < 1 || v > 32) return set_error(ARA_E_ARG, "round trigger in [1, 32]");
+      c->round_min = (int)v;
+      return ARA_OK;
+    case ARA_OPT_STREAM: {
+      int n = 0;
+      stream_variants(&n);
+      if (v < 0 || v > n) return set_error(ARA_E_ARG, "stream kernel in [0, %d]", n);
+      c->stream_kernel = (int)v;
+      return ARA_OK;
+    }
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }
@@ -872,6 +1010,8 @@ ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
     case ARA_OPT_PREFETCH: *v = c->prefetch; return ARA_OK;
     case ARA_OPT_FILTER: *v = c->filter; return ARA_OK;
     case ARA_OPT_PRECOMBINED: *v = c->precombined; return ARA_OK;
+    case ARA_OPT_STREAM: *v = c->stream_kernel; return ARA_OK;
+    case ARA_OPT_ROUND_MIN: *v = c->round_min; return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }
@@ -920,6 +1060,8 @@ const char* ara_status_string(ara_status s) {
 }
 
 const char* ara_last_error(void) { return g_err; }
+
+const char* ara_kernel_name(ara_ctx* c) { return c ? c->last_kernel : ""; }
 
 uint32_t ara_version(void) { return (ARA_VERSION_MAJOR << 16) | ARA_VERSION_MINOR; }
 

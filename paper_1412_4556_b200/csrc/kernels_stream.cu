@@ -1,0 +1,21 @@
+// kernels_stream.cu -- instantiations of the fixed-length-trial ARA kernels: the per-lane-queue kernel
+// (lane_kernel.cuh, default) and the warp-ring kernel (stream_kernel.cuh, kept for comparison).
+#include "lane_kernel.cuh"
+#include "stream_kernel.cuh"
+#include "variants.cuh"
+
+namespace ara {
+
+#define ARA_LANE(NW_) \
+  {NW_, ara_lane_kernel<NW_, false>, ara_lane_kernel<NW_, true>, "ara_lane_kernel<NW=" #NW_ ">", 0}
+#define ARA_RING(NW_) \
+  {NW_, ara_stream_kernel<NW_, false>, ara_stream_kernel<NW_, true>, "ara_stream_kernel<NW=" #NW_ ">", 1}
+
+static const StreamVariant kStream[] = {ARA_LANE(32), ARA_LANE(24), ARA_LANE(16), ARA_RING(32)};  // first = default
+
+const StreamVariant* stream_variants(int* n) {
+  *n = (int)(sizeof(kStream) / sizeof(kStream[0]));
+  return kStream;
+}
+
+}  // namespace ara

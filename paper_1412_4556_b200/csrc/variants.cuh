@@ -30,4 +30,13 @@ const Variant* presence_variants_mid(int* n);     // 17..72 columns
 const Variant* presence_variants_wide(int* n);    // 73..128 columns
 const Variant* dense_variants(int* n);
 
+// Fixed-length-trial kernel (stream_kernel.cuh): one instantiation serves every row width.
+struct StreamVariant {
+  int NW;
+  KernelFn fn, fn_olt;
+  const char* name;
+  int ring;  // 0: per-lane queues (lane_kernel.cuh), 1: warp hit ring (stream_kernel.cuh)
+};
+const StreamVariant* stream_variants(int* n);  // kernels_stream.cu; first = default
+
 }  // namespace ara

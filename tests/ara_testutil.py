@@ -43,8 +43,8 @@ def gpu_ylt(cfg_or_none, ctx, event_ids_np, offsets_np=None, K=0, num_trials=Non
         n = num_trials if num_trials is not None else (ids.numel() // K if K else 0)
     ylt = torch.full((num_layers, max(n, 1)), -7.0, dtype=torch.float64, device=dev)
     if kernel is not None:
-        ctx.ara_set_option(ara.ARA_OPT_KERNEL, kernel)
-    if variant is not None:
+        select(ctx, kernel, variant if variant is not None else 0)
+    elif variant is not None:
         ctx.ara_set_option(ara.ARA_OPT_VARIANT, variant)
     if block_threads is not None:
         ctx.ara_set_option(ara.ARA_OPT_BLOCK_THREADS, block_threads)
@@ -80,12 +80,33 @@ def within_tol(gpu, ref, rel=1e-6, abs_floor=1e-3):
     return np.abs(gpu - ref) <= np.maximum(rel * np.abs(ref), abs_floor)
 
 
+KERNEL_STREAM = 2       # test-level selector: the presence path with the fixed-length stream kernel
+STREAM_VARIANTS = 4     # ARA_OPT_STREAM = 1..4 (lane kernel 32, 24, 16 warps per block; ring kernel)
+
+
+def select(ctx, kernel, variant=0):
+    """Select a kernel for the next runs: KERNEL_PRESENCE / KERNEL_DENSE variant v with the stream kernel
+    off, KERNEL_STREAM = the presence path with stream variant v (it applies to fixed-length YETs with
+    K % 4 == 0 and 16-B aligned ids, else the presence kernel runs), KERNEL_AUTO = library defaults."""
+    from paper_1412_4556_b200 import ara
+    if kernel == KERNEL_STREAM:
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+        ctx.ara_set_option(ara.ARA_OPT_STREAM, variant + 1)
+        return
+    ctx.ara_set_option(ara.ARA_OPT_KERNEL, kernel)
+    ctx.ara_set_option(ara.ARA_OPT_STREAM, 1 if kernel == ara.KERNEL_AUTO else 0)
+    if kernel != ara.KERNEL_AUTO:
+        ctx.ara_set_option(ara.ARA_OPT_VARIANT, variant)
+
+
 def variants(ctx):
-    """All (kernel, variant) pairs the context can run for its layers' row width."""
+    """All (kernel, variant) pairs the context can run for its layers' row width (stream variants
+    included), leaving the context on the library defaults."""
     from paper_1412_4556_b200 import ara
     out = []
     for k in (ara.KERNEL_PRESENCE, ara.KERNEL_DENSE):
-        ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
+        select(ctx, k, 0)
         out += [(k, v) for v in range(ctx.ara_layer_info(0)["num_variants"])]
-    ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_AUTO)
+    out += [(KERNEL_STREAM, v) for v in range(STREAM_VARIANTS)]
+    select(ctx, ara.KERNEL_AUTO)
     return out

@@ -12,7 +12,8 @@ import pytest
 import torch
 
 import oracle
-from ara_testutil import gpu_ylt, golden, golden_context, golden_elts, golden_layer, ragged, variants, within_tol
+from ara_testutil import (KERNEL_STREAM, gpu_ylt, golden, golden_context, golden_elts, golden_layer, ragged, select,
+                          variants, within_tol)
 from paper_1412_4556_b200 import ara, synth
 
 pytestmark = pytest.mark.gpu
@@ -349,13 +350,19 @@ def test_metrics_match_oracle(cuda_device, case):
 
 
 # ------------------------------------------------------------------ fake multi-GPU (shards on one GPU)
-def test_sharded_runs_reassemble_bitwise(cuda_device):
+@pytest.mark.parametrize("name", ["T", "V"])
+def test_sharded_runs_reassemble_bitwise(cuda_device, name):
+    """Shards run one after another on one GPU (each its own YET buffer, as on G GPUs), reassembled by
+    ara_unshard: equal to the oracle over the whole YET (bitwise in the integer regime T, within the
+    north_star tolerance in the real regime V) and bitwise to the unsharded GPU run."""
     from paper_1412_4556_b200 import dist
-    cfg = synth.Config.load("V")
+    cfg = synth.Config.load(name)
     elts = synth.make_elts(cfg)
     full = synth.make_yet(cfg)
+    want = oracle.ylt_for(cfg, elts, full)
     ctx = ara.context_for_config(cfg, elts)
-    want = gpu_ylt(cfg, ctx, full.event_ids, offsets_np=full.offsets)
+    single = gpu_ylt(cfg, ctx, full.event_ids, offsets_np=full.offsets, K=full.events_per_trial,
+                     num_trials=full.num_trials)
     for G in (2, 3, 8):
         starts = dist.shard_starts(cfg.num_trials, G)
         cap = dist.shard_cap(cfg.num_trials, G)
@@ -363,11 +370,17 @@ def test_sharded_runs_reassemble_bitwise(cuda_device):
         for g in range(G):
             y = synth.make_yet(cfg, starts[g], starts[g + 1])
             gathered[g, :, :starts[g + 1] - starts[g]] = torch.from_numpy(
-                gpu_ylt(cfg, ctx, y.event_ids, offsets_np=y.offsets)).cuda()
+                gpu_ylt(cfg, ctx, y.event_ids, offsets_np=y.offsets, K=y.events_per_trial,
+                        num_trials=y.num_trials)).cuda()
         out = torch.empty((1, cfg.num_trials), dtype=torch.float64, device=cuda_device)
         ara.ara_unshard(gathered, G, cap, 1, starts, out)
         torch.cuda.synchronize()
-        assert np.array_equal(out.cpu().numpy(), want), G
+        got = out.cpu().numpy()
+        if cfg.regime == "integer":
+            assert np.array_equal(got, want), G
+        else:
+            assert np.all(within_tol(got, want)), G
+        assert np.array_equal(got, single), G
 
 
 # ------------------------------------------------------------------ presence kernel specifics
@@ -528,8 +541,7 @@ def test_olt_matches_oracle_every_kernel(cuda_device, name):
     ids = torch.from_numpy(yet.event_ids.view(np.int32)).cuda()
     off = None if yet.offsets is None else torch.from_numpy(yet.offsets.view(np.int64)).cuda()
     for k, v in variants(ctx):
-        ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
-        ctx.ara_set_option(ara.ARA_OPT_VARIANT, v)
+        select(ctx, k, v)
         y = torch.zeros((1, yet.num_trials), dtype=torch.float64, device=cuda_device)
         o = torch.full((1, yet.num_trials), -1.0, dtype=torch.float64, device=cuda_device)
         ctx.ara_run_ex(ids, y, o, offsets=off, events_per_trial=yet.events_per_trial, num_trials=yet.num_trials)
@@ -547,8 +559,7 @@ def test_olt_wide_rows_and_empty_trials(cuda_device):
     wy, wo = oracle.ylt_olt(C, ids, off, len(trials), 0, elts, [layer])
     ctx = _ctx_from(C, elts, [layer])
     for k, v in variants(ctx):
-        ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
-        ctx.ara_set_option(ara.ARA_OPT_VARIANT, v)
+        select(ctx, k, v)
         y = torch.zeros((1, len(trials)), dtype=torch.float64, device=cuda_device)
         o = torch.full((1, len(trials)), -1.0, dtype=torch.float64, device=cuda_device)
         ctx.ara_run_ex(torch.from_numpy(ids.view(np.int32)).cuda(), y, o,
@@ -600,8 +611,8 @@ def test_multi_layer_mixed_widths_with_olt_every_kernel(cuda_device):
     wy, wo = oracle.ylt_olt(C, yet, None, N, K, elts, layers)
     ctx = _ctx_from(C, elts, layers)
     ids = torch.from_numpy(yet.view(np.int32)).cuda()
-    for k in (ara.KERNEL_AUTO, ara.KERNEL_PRESENCE, ara.KERNEL_DENSE):
-        ctx.ara_set_option(ara.ARA_OPT_KERNEL, k)
+    for k in (ara.KERNEL_AUTO, ara.KERNEL_PRESENCE, ara.KERNEL_DENSE, KERNEL_STREAM):
+        select(ctx, k)
         y = torch.zeros((len(layers), N), dtype=torch.float64, device=cuda_device)
         o = torch.zeros((len(layers), N), dtype=torch.float64, device=cuda_device)
         ctx.ara_run_ex(ids, y, o, events_per_trial=K, num_trials=N)

@@ -1,0 +1,151 @@
+"""GPU parity of the fixed-length-trial stream kernel (csrc/stream_kernel.cuh) against the CPU oracle.
+
+The stream kernel is the default ARA path for YETs of fixed-length trials (K % 4 == 0, 16-B aligned ids:
+configs P, PI, M, X).  It must give
+  * the oracle's YLT BITWISE in the integer regime (every fp64 operation exact), and
+    within the north_star tolerance otherwise;
+  * the presence kernel's YLT bitwise in every regime (same per-trial summation order), for every
+    variant and any trial sharding.
+Shapes cover trials much shorter than a batch (K = 4: a batch spans many trials), runs of more than 32
+trials without hits (the register ring overflow path), windows with a lane-masked tail (K % 128 != 0),
+single-window trials, invalid ids and the occurrence loss table.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from ara_testutil import KERNEL_STREAM, STREAM_VARIANTS, gpu_ylt, select, within_tol
+from paper_1412_4556_b200 import ara, synth
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+FIXED_KERNELS = ("ara_lane_kernel", "ara_stream_kernel")
+LANE_VARIANTS = (0, 1, 2)  # ARA_OPT_STREAM - 1 of the per-lane-queue kernel (32, 24, 16 warps per block)
+RING_VARIANT = 3           # the warp-ring kernel
+
+
+def _problem(J, C, n, K, N, integer=True, seed=0, sparse_yet=False):
+    rng = np.random.default_rng(seed + 7919 * J + K)
+    elts = []
+    for j in range(J):
+        ids = rng.choice(np.arange(1, C + 1), size=n, replace=False).astype(np.uint32)
+        losses = (rng.integers(1, 1 << 20, size=n) if integer else rng.random(n) * 1e6 + 0.5).astype(np.float32)
+        r = float(rng.integers(0, 1 << 18)) if integer else float(rng.integers(0, 1 << 18)) + 0.25
+        lim = INF if j % 3 == 1 else float(rng.integers(1 << 18, 1 << 21))
+        elts.append((ids, losses, (r, lim)))
+    yet = rng.integers(1, C + 1, size=N * K).astype(np.uint32)
+    if sparse_yet:  # long runs of trials whose events are absent from every ELT
+        present = np.zeros(C + 1, bool)
+        for ids, _, _ in elts:
+            present[ids] = True
+        absent = np.flatnonzero(~present[1:]) + 1
+        run = rng.random(N) < 0.85
+        for t in np.flatnonzero(run):
+            yet[t * K:(t + 1) * K] = rng.choice(absent, size=K)
+    layer = (list(range(J)), (5000.0, float(1 << 22)), (2e5, 4e6))
+    return elts, layer, yet
+
+
+def _ctx(C, elts, layers):
+    return ara.Context(C, [ara.Elt(i, l, r, lim) for i, l, (r, lim) in elts],
+                       [ara.Layer(idx, a[0], a[1], b[0], b[1]) for idx, a, b in layers])
+
+
+@pytest.mark.parametrize("K", [4, 8, 12, 100, 128, 132, 256, 1000])
+def test_stream_bitwise_integer_regime(cuda_device, K):
+    C, J = 20_000, 16
+    N = max(64, 600_000 // K // 10)
+    elts, layer, yet = _problem(J, C, 800, K, N)
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx(C, elts, [layer])
+    for v in range(STREAM_VARIANTS):
+        got = gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=v)
+        assert ctx.ara_kernel_name().startswith(FIXED_KERNELS), ctx.ara_kernel_name()
+        assert np.array_equal(got, want), (K, v)
+
+
+@pytest.mark.parametrize("K", [4, 16, 132])
+def test_stream_hitless_runs(cuda_device, K):
+    """85% of the trials draw only events absent from every ELT: runs far longer than the 32-trial
+    register ring, so the kernel must flush and close them (YLT +0) without losing the others."""
+    C, J = 50_000, 4
+    N = 20_000
+    elts, layer, yet = _problem(J, C, 300, K, N, sparse_yet=True)
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    assert (want == 0).mean() > 0.8
+    ctx = _ctx(C, elts, [layer])
+    for v in range(STREAM_VARIANTS):
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=v), want), v
+
+
+@pytest.mark.parametrize("J", [1, 2, 3, 16, 17, 100, 128])
+def test_stream_equals_presence_real_regime(cuda_device, J):
+    """Real-valued losses and terms, also for a catalogue larger than the shared bitmap (folded):
+    * the warp-ring kernel sums a trial's hits in the presence kernel's order: bitwise equal to it;
+    * the per-lane-queue kernel sums by position class: bitwise equal across its variants (the order
+      does not depend on the launch shape or the fold) and within 1e-12 relative of the presence kernel;
+    * all of them within the north_star tolerance of the oracle."""
+    for C, n, K, N in ((30_000, 1500, 1000, 3000), (3_000_000, 20_000, 1000, 2000)):
+        elts, layer, yet = _problem(J, C, n, K, N, integer=False, seed=5)
+        want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+        ctx = _ctx(C, elts, [layer])
+        pres = gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=ara.KERNEL_PRESENCE, variant=0)
+        assert ctx.ara_kernel_name().startswith("ara_presence_kernel")
+        ring = gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=RING_VARIANT)
+        assert ctx.ara_kernel_name().startswith("ara_stream_kernel")
+        assert np.array_equal(ring, pres), (J, C)
+        lanes = [gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=v) for v in LANE_VARIANTS]
+        assert ctx.ara_kernel_name().startswith("ara_lane_kernel")
+        for y in lanes[1:]:
+            assert np.array_equal(y, lanes[0]), (J, C)
+        assert np.all(within_tol(lanes[0], pres, rel=1e-12, abs_floor=1e-6)), (J, C)
+        assert np.all(within_tol(pres, want)) and np.all(within_tol(lanes[0], want)), (J, C)
+
+
+def test_stream_sharding_invariant_and_vs_oracle(cuda_device):
+    """Trial blocks of a sharded run (each shard its own YET buffer, as on G GPUs) reassemble to the
+    unsharded YLT bitwise, and both equal the oracle within tolerance (real regime)."""
+    cfg = synth.Config.load("P")
+    elts = synth.make_elts(cfg)
+    N, K = 12_000, cfg.kmin
+    ids = synth.yet_ids(cfg.seed, cfg.catalog_size, 0, N * K)
+    ctx = ara.context_for_config(cfg, elts)
+    select(ctx, ara.KERNEL_AUTO)
+    whole = gpu_ylt(None, ctx, ids, K=K, num_trials=N)
+    assert ctx.ara_kernel_name().startswith("ara_lane_kernel")  # the default for fixed-length trials
+    for G in (2, 3, 8):
+        starts = [(g * N) // G for g in range(G + 1)]
+        parts = [gpu_ylt(None, ctx, ids[starts[g] * K:starts[g + 1] * K], K=K, num_trials=starts[g + 1] - starts[g])
+                 for g in range(G)]
+        assert np.array_equal(np.concatenate(parts, axis=1), whole), G
+    sample = np.arange(0, N, 7)
+    want = oracle.ylt_for(cfg, elts, synth.make_yet_trials(cfg, sample))
+    assert np.all(within_tol(whole[:, sample], want))
+
+
+def test_stream_olt_and_invalid_ids(cuda_device):
+    C, J, K, N = 20_000, 16, 1000, 500
+    elts, layer, yet = _problem(J, C, 800, K, N, seed=3)
+    wy, wo = oracle.ylt_olt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx(C, elts, [layer])
+    ids = torch.from_numpy(yet.view(np.int32)).cuda()
+    for v in range(STREAM_VARIANTS):
+        select(ctx, KERNEL_STREAM, v)
+        y = torch.zeros((1, N), dtype=torch.float64, device=cuda_device)
+        o = torch.full((1, N), -1.0, dtype=torch.float64, device=cuda_device)
+        ctx.ara_run_ex(ids, y, o, events_per_trial=K, num_trials=N)
+        ctx.ara_check()
+        assert ctx.ara_kernel_name().startswith(FIXED_KERNELS)
+        assert np.array_equal(y.cpu().numpy(), wy) and np.array_equal(o.cpu().numpy(), wo), v
+    for bad in (0, C + 1, 2**32 - 1):
+        b = yet.copy()
+        b[K * 123 + 17] = bad
+        select(ctx, KERNEL_STREAM, 0)
+        with pytest.raises(ara.AraError) as e:
+            gpu_ylt(None, ctx, b, K=K, num_trials=N)
+        assert e.value.status == ara.ARA_E_RANGE
+        # a valid run afterwards is clean again
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N), wy)

@@ -333,3 +333,20 @@ def test_aal_and_ep_examples():
     assert list(oracle.ep(np.array(g["ep_losses"]), g["ep_thresholds"])) == g["ep_probs"]
     y = np.array([0.0, 5.0, 5.0, 7.0])
     assert oracle.aal(y) == 4.25 and list(oracle.ep(y, [5.0, 5.1, 0.0])) == [0.75, 0.25, 1.0]
+
+
+def test_layer_totals_hand_worked():
+    """Program / portfolio totals, worked by hand: three layers, two groups.
+    The third trial pins the summation order (layer order): fl(fl(1e16 + 1) + 1) = 1e16 (ulp(1e16) = 2,
+    ties to even), whereas summing the two 1's first would give 1e16 + 2."""
+    ylt = np.array([[1.0, 2.0, 1e16],
+                    [10.0, 20.0, 7.0],
+                    [100.0, 200.0, 1.0],
+                    [0.0, 0.5, 1.0]])
+    group = [0, 1, 0, 0]
+    got = oracle.layer_totals(ylt, group, 2)
+    assert np.array_equal(got, np.array([[101.0, 202.5, 1e16],
+                                         [10.0, 20.0, 7.0]]))
+    assert 1e16 + 2.0 != 1e16  # the alternative order is distinguishable
+    # a group with no layer is all zero; one group is the column sum of a small integer matrix
+    assert np.array_equal(oracle.layer_totals(ylt[:2, :2], [1, 1], 3), np.array([[0.0, 0.0], [11.0, 22.0], [0.0, 0.0]]))
