@@ -53,6 +53,8 @@ def parse():
                     help="ARA_OPT_STREAM: 0 = presence kernel for fixed-length trials, 1..3 = stream kernel variant")
     ap.add_argument("--prefetch", type=int, default=None, choices=[-1, 0, 1], help="ARA_OPT_PREFETCH")
     ap.add_argument("--round-min", type=int, default=None, help="ARA_OPT_ROUND_MIN (lane kernel round trigger)")
+    ap.add_argument("--trial-order", type=int, default=None, choices=[0, 1], help="ARA_OPT_TRIAL_ORDER")
+    ap.add_argument("--eager", action="store_true", help="issue the step's calls one by one (no captured plan)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cold", action="store_true")
@@ -283,6 +285,8 @@ def main():
         ctx.ara_set_option(ara.ARA_OPT_PREFETCH, args.prefetch)
     if args.round_min is not None:
         ctx.ara_set_option(ara.ARA_OPT_ROUND_MIN, args.round_min)
+    if args.trial_order is not None:
+        ctx.ara_set_option(ara.ARA_OPT_TRIAL_ORDER, args.trial_order)
     info = [ctx.ara_layer_info(l) for l in range(L)]
 
     # ---- this rank's YET shard, generated in HBM
@@ -300,26 +304,42 @@ def main():
     n_ids = q1 - q0
     ids = torch.empty(n_ids, dtype=torch.int32, device=dev)
     synth.yet_ids_device(ids.data_ptr(), cfg.seed, cfg.catalog_size, q0, n_ids, sp)
-    ylt_local = torch.empty((L, n_local), dtype=torch.float64, device=dev)
     rps = synth.return_periods(N)
     m = len(rps)
-    met = torch.empty((L, 2, max(m, 1)), dtype=torch.float64, device=dev)  # per layer: PML row, TVaR row
+    met = torch.zeros((L, 2, max(m, 1)), dtype=torch.float64, device=dev)  # per layer: PML row, TVaR row
     met_h = torch.empty((L, 2, max(m, 1)), dtype=torch.float64, pin_memory=True)
+    gat = adist.YltGather(L, N, dev) if world > 1 else None
+    ylt_local = gat.local if gat is not None else torch.empty((L, n_local), dtype=torch.float64, device=dev)
+    pml_dev = torch.zeros((L, max(m, 1)), dtype=torch.float64, device=dev)
+    tvar_dev = torch.zeros((L, max(m, 1)), dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
 
+    # ara_run over every layer is captured once (ara_plan_create: one CUDA graph, launch attributes and
+    # folds set up beforehand), so the timed loop issues one graph launch per step for it; the CUDA events
+    # around that launch time the ARA kernels alone.  --eager issues ara_run directly.
+    plan = None
+    if not args.eager:
+        plan = ctx.ara_plan_create(ids, ylt_local, [], None, None, offsets=offsets_d, events_per_trial=K,
+                                   num_trials=n_local, stream=stream)
+
     def step(evs=None):
-        """One pass of the hot path: ara_run (all layers) -> [all-gather] -> PML/TVaR per layer, the
-        metrics enqueued asynchronously into device buffers and copied to pinned host memory on the
-        same stream, so consecutive steps pipeline without a host round trip."""
+        """One pass of the hot path: ara_run (all layers) -> [all-gather] -> PML/TVaR per layer (on rank 0
+        when sharded), results copied to pinned host memory on the same stream (no host round trip)."""
         if evs is not None:
             evs[0].record(stream)
-        ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        if plan is not None:
+            plan.launch(stream=stream)
+        else:
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
         if evs is not None:
             evs[1].record(stream)
-        full = adist.gather_ylt(ylt_local, N) if world > 1 else ylt_local
-        if m:
+        full = gat.gather(stream=stream) if world > 1 else ylt_local
+        if m and (world == 1 or rank == 0):
             for l in range(L):
-                ara.ara_pml_tvar_device(full[l], rps, met[l, 0], met[l, 1], stream=stream)
+                ara.ara_pml_tvar_device(full[l], rps, pml_dev[l], tvar_dev[l], stream=stream)
+        if m and (world == 1 or rank == 0):
+            met[:, 0].copy_(pml_dev, non_blocking=True)
+            met[:, 1].copy_(tvar_dev, non_blocking=True)
             met_h.copy_(met, non_blocking=True)
         return full
 
@@ -327,7 +347,7 @@ def main():
     full = step()
     ctx.ara_check(stream)
     torch.cuda.synchronize()
-    for l in range(L if m else 0):  # the asynchronous metrics equal the synchronous API's
+    for l in range(L if m and (world == 1 or rank == 0) else 0):  # the captured/async metrics equal the sync API's
         p_sync, t_sync = ara.ara_pml_tvar(full[l], rps, stream=stream)
         if not (np.array_equal(p_sync, met_h[l, 0].numpy()) and np.array_equal(t_sync, met_h[l, 1].numpy())):
             print(json.dumps({"error": f"layer {l}: ara_pml_tvar_device != ara_pml_tvar"}), flush=True)
@@ -468,7 +488,7 @@ def main():
     peak, peak_src = peaks()
     kernel_full = ctx.ara_kernel_name()  # the kernel the timed runs launched
     kernel_name = kernel_full.split("<")[0]
-    sparse_path = kernel_name in ("ara_presence_kernel", "ara_stream_kernel")
+    sparse_path = kernel_name in ("ara_presence_kernel", "ara_stream_kernel", "ara_lane_kernel")
     # compulsory HBM bytes of one presence-kernel launch: the YET ids (4 B per occurrence), the YLT
     # row (8 B per trial), and one read of every table row that holds a loss plus the bitmap
     present_rows = [ctx.ara_layer_stats(l)["present_rows"] for l in range(L)]
@@ -522,7 +542,7 @@ def main():
         ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
         ref_ylt = ylt_local.clone()  # the product path's YLT
         # the round-1 presence kernel (stream kernel off), timed beside: its YLT must equal bit for bit
-        if kernel_name == "ara_stream_kernel":
+        if kernel_name in ("ara_stream_kernel", "ara_lane_kernel"):
             ctx.ara_set_option(ara.ARA_OPT_STREAM, 0)
             for _ in range(2):
                 ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
@@ -639,12 +659,12 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
     from paper_1412_4556_b200 import ara
     rb = max(32, info[0]["row_stride"])
     if info[0].get("product_kernel", "").startswith(("ara_stream", "ara_lane")):  # fixed-length-trial kernels
-        for sv in (1, 2, 3, 4):
+        for sv in (1, 4):
             for pf in (0, 1):
-                for pol in (0, 1):
+                for pol in (0, 1):  # here: the trial order (0 blocks, 1 interleaved)
                     ctx.ara_set_option(ara.ARA_OPT_STREAM, sv)
                     ctx.ara_set_option(ara.ARA_OPT_PREFETCH, pf)
-                    ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, pol)
+                    ctx.ara_set_option(ara.ARA_OPT_TRIAL_ORDER, pol)
                     for _ in range(2):
                         ctx.ara_run(ids, ylt_local, offsets=None, events_per_trial=K, num_trials=n_local, stream=stream)
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -653,11 +673,10 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
                         ctx.ara_run(ids, ylt_local, offsets=None, events_per_trial=K, num_trials=n_local, stream=stream)
                     b.record(stream)
                     torch.cuda.synchronize()
-                    print(json.dumps({"sweep": ctx.ara_kernel_name(), "prefetch": pf, "l2_policy": pol,
+                    print(json.dumps({"sweep": ctx.ara_kernel_name(), "prefetch": pf, "trial_order": pol,
                                       "launch_ms": a.elapsed_time(b) / 5 / L}), file=sys.stderr, flush=True)
-        ctx.ara_set_option(ara.ARA_OPT_STREAM, 1)
-        ctx.ara_set_option(ara.ARA_OPT_PREFETCH, 0)
-        ctx.ara_set_option(ara.ARA_OPT_L2_POLICY, 0)
+        ctx.ara_set_option(ara.ARA_OPT_PREFETCH, -1)
+        ctx.ara_set_option(ara.ARA_OPT_TRIAL_ORDER, 1)
         ctx.ara_set_option(ara.ARA_OPT_STREAM, 0)  # then the presence kernel's own sweep
     nv = info[0]["num_variants"]
     presence = info[0]["variant"].startswith("ara_presence")

@@ -125,6 +125,21 @@ ARA_API ara_status ara_run(ara_ctx* ctx, const ara_yet* yet, double* ylt, void* 
  * (SURVEY.md N4).  Same conventions and errors as ara_run. */
 ARA_API ara_status ara_run_ex(ara_ctx* ctx, const ara_yet* yet, double* ylt, double* olt, void* stream);
 
+/* A captured analysis step for repeated runs over the same device buffers (PAPER.md:230 times many runs
+ * of one workload): ara_run over `yet` (DEVICE, borrowed) into ylt, then PML/TVaR of every layer at the
+ * m return periods into pml_dev / tvar_dev (DEVICE, [num_layers][m] each, either may be NULL; m = 0:
+ * no metrics).  ara_plan_create runs the step once eagerly (building every cached structure and
+ * validating the arguments), then records it into a CUDA graph with all scratch preallocated;
+ * ara_plan_launch replays it on `stream` with one graph launch (asynchronous; the results are the
+ * same as the eager calls, bit for bit).  The buffers must stay alive until ara_plan_destroy.  Invalid
+ * ids are reported by ara_check as for ara_run.  Errors: as ara_run and ara_pml_tvar_device, plus
+ * ARA_E_CUDA when the graph cannot be captured. */
+typedef struct ara_plan ara_plan;
+ARA_API ara_status ara_plan_create(ara_ctx* ctx, const ara_yet* yet, double* ylt, const double* rps, uint32_t m,
+                                   double* pml_dev, double* tvar_dev, void* stream, ara_plan** out);
+ARA_API ara_status ara_plan_launch(ara_plan* plan, void* stream);
+ARA_API void ara_plan_destroy(ara_plan* plan); /* NULL is a no-op */
+
 /* End-to-end variant for a HOST YET (pinned memory gives copy/compute overlap; pageable works but
  * serialises): the YET is streamed to the device in trial batches on an internal copy stream,
  * overlapped with the analysis of the previous batch, and the YLT is written to HOST ylt_host
@@ -194,14 +209,15 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
                        const uint64_t* starts, double* ylt, void* stream);
 
 /* Tuning knobs (launch-shape sweep; L2 policy).  0 = library default.
- *   ARA_OPT_BLOCK_THREADS   threads per block (multiple of 32, <= 1024)
+ *   ARA_OPT_BLOCK_THREADS   threads per block of the dense kernel (multiple of 32, 32..256)
  *   ARA_OPT_BLOCKS_PER_SM   resident blocks per SM the persistent grid is sized for
  *   ARA_OPT_L2_POLICY       0 default (evict_last hints on table rows and records; the dense kernel
  *                           also marks YET ids evict_first), 1 no hints, 2 hints + persisting
  *                           access-policy window on the table
- *   ARA_OPT_PREFETCH        presence kernel: 1 each warp prefetches its next trial's ids into L2 at
- *                           the start of a trial, 0 (default) off -- every window, the trial's first
- *                           and last included, is already requested one step ahead in registers
+ *   ARA_OPT_PREFETCH        L2 prefetch of the YET ahead of the register-staged windows: -1 auto
+ *                           (default: on for the fixed-length-trial kernels -- one bulk prefetch of the
+ *                           trial after next per trial --, off for the presence kernel), 0 off, 1 on
+ *                           (presence kernel: each warp prefetches its next trial at a trial start)
  *   ARA_OPT_VARIANT         kernel variant index within the selected kernel and row width
  *                           (ara_layer_info reports the count)
  *   ARA_OPT_KERNEL          -1 auto (default): per layer, the presence kernel when its folded bitmap is
@@ -211,8 +227,10 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           dense kernel;
  *                           0 presence: a per-layer presence bitmap of the table's non-zero rows,
  *                           staged in shared memory, so only rows that hold a loss are gathered;
- *                           1 dense: every occurrence gathers its full row.  Identical results (an
- *                           all-zero row contributes exactly 0, reading c9).
+ *                           1 dense: every occurrence gathers its full row.  The same YLT up to
+ *                           the fp64 summation order (an all-zero row contributes exactly 0, PAPER.md:209,
+ *                           reading c9): bitwise identical in the integer regime, within ~1e-12
+ *                           relative otherwise (each kernel's order is fixed, so each is reproducible).
  *                           Selecting a kernel resets ARA_OPT_VARIANT to 0.
  *   ARA_OPT_FILTER          presence kernel, one lane per row: -1 auto (default; = off), 0 off, 1 on.
  *                           The exact filter stage checks every candidate of the folded shared-memory
@@ -226,11 +244,19 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           YLT; exact only for deterministic losses (no secondary uncertainty,
  *                           PAPER.md:125), and no ELT lookups happen at run time.
  *   ARA_OPT_STREAM          1 (default): for a YET of fixed-length trials (no offsets, K % 4 == 0, 16-B
- *                           aligned ids) the presence path runs the stream kernel (stream_kernel.cuh:
- *                           contiguous trial blocks per warp, a register-held trial ring, fewer
- *                           instructions per occurrence); v = 1..3 selects its variant (32, 24, 16 warps
- *                           per block); 0 = always the presence kernel.  Bitwise identical YLT (the same
- *                           per-trial summation order).
+ *                           aligned ids, catalogue < 2^32 - 2) the presence path runs a fixed-length-
+ *                           trial kernel: v = 1..3 the per-lane-queue kernel (lane_kernel.cuh: each
+ *                           lane queues the hits of its own window positions and sums them in stream
+ *                           order; 32, 24, 16 warps per block; the default), v = 4 the warp-ring
+ *                           kernel (stream_kernel.cuh: the presence kernel's summation order); 0 =
+ *                           always the presence kernel.  Every kernel's order is fixed: the YLT is
+ *                           reproducible bit for bit and independent of the sharding; across kernels it
+ *                           agrees bitwise in the integer regime and within ~1e-12 relative otherwise.
+ *   ARA_OPT_ROUND_MIN       per-lane-queue kernel: a gather round starts when at least this many lanes
+ *                           hold a queued hit (1..32, 0 = default 24), or when a queue nearly fills.
+ *   ARA_OPT_TRIAL_ORDER     fixed-length-trial kernels: 1 (default) trials interleaved over the grid's
+ *                           warps (warp w takes trials w, w + W, ...: all warps stream one compact
+ *                           region of the YET), 0 contiguous trial blocks per warp.  Same YLT bits.
  * ARA_OPT_BLOCK_THREADS applies to the dense kernel; the presence kernel fixes its block size. */
 typedef enum {
   ARA_OPT_BLOCK_THREADS = 1,
@@ -242,7 +268,8 @@ typedef enum {
   ARA_OPT_FILTER = 7,
   ARA_OPT_PRECOMBINED = 8,
   ARA_OPT_STREAM = 9,
-  ARA_OPT_ROUND_MIN = 10
+  ARA_OPT_ROUND_MIN = 10,
+  ARA_OPT_TRIAL_ORDER = 11
 } ara_option;
 ARA_API ara_status ara_set_option(ara_ctx* ctx, ara_option opt, int64_t value);
 ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);

@@ -27,6 +27,7 @@ ARA_OPT_FILTER = 7
 ARA_OPT_PRECOMBINED = 8
 ARA_OPT_STREAM = 9
 ARA_OPT_ROUND_MIN = 10
+ARA_OPT_TRIAL_ORDER = 11
 KERNEL_AUTO, KERNEL_PRESENCE, KERNEL_DENSE = -1, 0, 1
 STUDY_INTERLEAVED, STUDY_INDEPENDENT, STUDY_SORTED = 0, 1, 2
 ARA_MAX_ELTS_PER_LAYER = 128
@@ -36,7 +37,7 @@ EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_ex", "ara_run_host",
            "ara_sum_layers", "ara_check", "ara_pml_tvar", "ara_pml",
            "ara_tvar", "ara_pml_tvar_device", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
            "ara_layer_info", "ara_layer_stats", "ara_table_row", "ara_kernel_name", "ara_status_string", "ara_last_error",
-           "ara_version")
+           "ara_version", "ara_plan_create", "ara_plan_launch", "ara_plan_destroy")
 
 
 class AraError(RuntimeError):
@@ -101,6 +102,9 @@ def lib() -> ctypes.CDLL:
                                      ctypes.POINTER(ctypes.c_int)]),
             "ara_table_row": (st, [vp, u32, u32, dp]),
             "ara_kernel_name": (ctypes.c_char_p, [vp]),
+            "ara_plan_create": (st, [vp, ctypes.POINTER(_Yet), dp, dp, u32, dp, dp, vp, ctypes.POINTER(vp)]),
+            "ara_plan_launch": (st, [vp, vp]),
+            "ara_plan_destroy": (None, [vp]),
             "ara_status_string": (ctypes.c_char_p, [ctypes.c_int]),
             "ara_last_error": (ctypes.c_char_p, []),
             "ara_version": (u32, []),
@@ -234,6 +238,19 @@ class Context:
         y = _yet_struct(event_ids, offsets, n, events_per_trial)
         _check(lib().ara_run(self._h, ctypes.byref(y), _dptr(ylt), _stream_ptr(stream)), "ara_run")
 
+    def ara_plan_create(self, event_ids, ylt, rps, pml_dev=None, tvar_dev=None, offsets=None,
+                        events_per_trial: int = 0, num_trials: Optional[int] = None, stream=None) -> "Plan":
+        """Capture one analysis step (ara_run + PML/TVaR of every layer into device [layers, m] buffers)
+        as a CUDA graph; returns a Plan whose launch() replays it.  The tensors must outlive the plan."""
+        n = num_trials if num_trials is not None else (offsets.numel() - 1 if offsets is not None else
+                                                       event_ids.numel() // max(1, events_per_trial))
+        y = _yet_struct(event_ids, offsets, n, events_per_trial)
+        r = np.ascontiguousarray(rps, dtype=np.float64)
+        h = ctypes.c_void_p()
+        _check(lib().ara_plan_create(self._h, ctypes.byref(y), _dptr(ylt), _dptr(r), r.size, _dptr(pml_dev),
+                                     _dptr(tvar_dev), _stream_ptr(stream), ctypes.byref(h)), "ara_plan_create")
+        return Plan(h, (event_ids, ylt, offsets, pml_dev, tvar_dev, r, self))
+
     def ara_run_ex(self, event_ids, ylt, olt=None, offsets=None, events_per_trial: int = 0,
                    num_trials: Optional[int] = None, stream=None) -> None:
         """ara_run plus the occurrence-basis table (largest occurrence-net loss per trial)."""
@@ -291,6 +308,28 @@ class Context:
         out = np.zeros(stride // 4, dtype=np.float32)
         _check(lib().ara_table_row(self._h, layer, event, _dptr(out)), "ara_table_row")
         return out
+
+
+class Plan:
+    """A captured analysis step (ara_plan_create); launch() = one CUDA graph launch."""
+
+    def __init__(self, handle, keep):
+        self._h = handle
+        self._keep = keep  # the buffers the graph reads and writes stay alive with the plan
+
+    def launch(self, stream=None) -> None:
+        _check(lib().ara_plan_launch(self._h, _stream_ptr(stream)), "ara_plan_launch")
+
+    def close(self) -> None:
+        if self._h:
+            lib().ara_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def _numel(a) -> int:

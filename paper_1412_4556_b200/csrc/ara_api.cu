@@ -74,6 +74,7 @@ struct Layer {
   };
   std::vector<Fold> folds;
   uint32_t fold_words = 0;  // canonical fold size of this layer (every presence/stream launch uses it)
+  bool xs_auto = false;     // fixed-length trials: the exact scan filter pays (ARA_OPT_FILTER auto)
   uint4* rec = nullptr;         // sparse row records (C + 2) x 16 B; record C + 1 is all zero (invalid ids)
   double* occ = nullptr;        // precombined o[e] per event, (C + 1) x 8 B, built on first use
   // Section IV.B study structures, built on first use by ara_run_study
@@ -115,8 +116,9 @@ struct ara_ctx {
   int precombined = 0;  // ARA_OPT_PRECOMBINED: 1 = gather o[e] from the precombined table
   int variant = 0;
   int kernel = -1;  // KernelKind, or -1 = per-layer automatic choice
+  int interleave = 1;     // ARA_OPT_TRIAL_ORDER: 1 trials interleaved over the warps, 0 contiguous blocks
   int round_min = 24;     // ARA_OPT_ROUND_MIN: lane kernel round trigger (lanes holding a queued hit)
-  int stream_kernel = 1;  // ARA_OPT_STREAM: 0 off, v > 0 = stream variant v - 1 for fixed-length trials
+  int stream_kernel = 0;  // ARA_OPT_STREAM: 0 off, v > 0 = stream variant v - 1 for fixed-length trials
   const char* last_kernel = "";  // name of the kernel the last launch used (layer 0)
   int persist_max = 0, window_max = 0;
   int smem_optin = 0;
@@ -365,8 +367,8 @@ static ara_status get_fold(ara_ctx* c, Layer& L, uint32_t words, cudaStream_t st
 // catalogue below 2^32 - 2 and per-warp hit ordinals that cannot wrap.
 static bool stream_eligible(const ara_ctx* c, const uint32_t* ids, const uint64_t* offsets, uint64_t num_trials,
                             uint32_t K, int nw) {
-  if (c->stream_kernel <= 0 || offsets || K == 0 || (K & 3u) || (reinterpret_cast<uintptr_t>(ids) & 15u)) return false;
-  if (c->filter == 1 || c->precombined) return false;  // those ablations live in the presence kernel
+  if (offsets || K == 0 || (K & 3u) || (reinterpret_cast<uintptr_t>(ids) & 15u)) return false;
+  if (c->precombined) return false;  // that ablation lives in the presence kernel
   if ((uint64_t)c->C + 2 > 0xffffffffull) return false;
   const uint64_t warps = (uint64_t)c->sms * nw;
   const uint64_t per_warp = (num_trials + warps - 1) / warps + 1;
@@ -409,6 +411,9 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   int nsv = 0;
   const StreamVariant* sv = stream_variants(&nsv);
   const StreamVariant* svar = (c->stream_kernel > 0 && c->stream_kernel <= nsv) ? &sv[c->stream_kernel - 1] : nullptr;
+  if (!svar && (c->filter == 1 || (c->filter < 0 && L.xs_auto)))  // exact scan filter for fixed-length trials
+    for (int v = 0; v < nsv && !svar; ++v)
+      if (sv[v].xs) svar = &sv[v];
   if (var->kind == KIND_PRESENCE && svar && stream_eligible(c, ids, offsets, num_trials, K, svar->NW)) {
     // fixed-length trials: the stream kernel (stream_kernel.cuh), one block of NW warps per SM
     fn = olt ? svar->fn_olt : svar->fn;
@@ -428,10 +433,12 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
     if (st) return st;
     p.present = fold;
     p.rec = L.rec;
+    p.exact = L.present;
     p.present_words = fw;
     p.fold_mul = mul;
     dyn_smem = (size_t)fw * 4 + extra;
     p.round_min = (uint32_t)c->round_min;
+    p.interleave = (uint32_t)c->interleave;
     st = fn_dyn_smem(c, (const void*)fn, dyn_smem);
     if (st) return st;
     bps = 1;
@@ -666,6 +673,11 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
         L.fold_words = (uint32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)pw, b / 4));
       }
       const double fw = budget > 0 ? std::min(pw, (double)L.fold_words) : 1.0;
+      {  // exact scan filter: the fold nominates at least twice the rows that hold a loss
+        const double d = (double)L.present_rows / ((double)catalog_size + 1.0);
+        const double cand = 1.0 - pow(1.0 - d, std::max(1.0, pw / fw));
+        L.xs_auto = cand >= 2.0 * d;
+      }
       const double dens = (double)L.present_rows / ((double)catalog_size + 1.0);
       L.est_hit_rate = 1.0 - pow(1.0 - dens, std::max(1.0, pw / fw));
       // The presence kernel pays off while it skips most rows.  With one lane per row (G = 1) a hit
@@ -740,6 +752,101 @@ ara_status ara_run_ex(ara_ctx* c, const ara_yet* yet, double* ylt, double* olt, 
 ara_status ara_run(ara_ctx* c, const ara_yet* yet, double* ylt, void* stream) {
   return ara_run_ex(c, yet, ylt, nullptr, stream);
 }
+
+}  // extern "C"
+
+// A captured analysis step: ara_run over a fixed device YET + PML/TVaR of every layer, replayed as one
+// CUDA graph (no per-step host work: launch attributes, folds and metric scratch are set up once).
+struct ara_plan {
+  int device = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  char* scratch = nullptr;
+};
+
+namespace ara {
+
+static ara_status plan_step(ara_ctx* c, const ara_yet* yet, double* ylt, const double* rps, uint32_t m,
+                            double* pml_dev, double* tvar_dev, char* scratch, size_t bytes, cudaStream_t s) {
+  ara_status st = run_layers(c, yet->event_ids, yet->trial_offsets, yet->num_trials, yet->num_events,
+                             yet->events_per_trial, ylt, nullptr, yet->num_trials, s);
+  if (st) return st;
+  for (size_t l = 0; m && l < c->layers.size(); ++l) {
+    st = metrics_device_into(ylt + l * yet->num_trials, yet->num_trials, rps, m, pml_dev ? pml_dev + l * m : nullptr,
+                             tvar_dev ? tvar_dev + l * m : nullptr, scratch, bytes, s);
+    if (st) return st;
+  }
+  return ARA_OK;
+}
+
+static void plan_free(ara_plan* p) {
+  if (!p) return;
+  DeviceGuard guard(p->device);
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  cudaFree(p->scratch);
+  delete p;
+}
+
+}  // namespace ara
+
+extern "C" {
+
+ara_status ara_plan_create(ara_ctx* c, const ara_yet* yet, double* ylt, const double* rps, uint32_t m,
+                           double* pml_dev, double* tvar_dev, void* stream, ara_plan** out) {
+  if (!c || !out) return set_error(ARA_E_ARG, "NULL argument");
+  *out = nullptr;
+  ara_status st = check_yet(yet);
+  if (st) return st;
+  if (yet->num_trials == 0 || !ylt) return set_error(ARA_E_ARG, "empty YET or NULL ylt");
+  if (m && (!rps || (!pml_dev && !tvar_dev))) return set_error(ARA_E_ARG, "metrics requested without outputs");
+  DeviceGuard guard(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  ara_plan* p = new (std::nothrow) ara_plan();
+  if (!p) return set_error(ARA_E_NOMEM, "host allocation failed");
+  p->device = c->device;
+  const size_t bytes = m ? metrics_scratch_size(yet->num_trials) : 0;
+  if (bytes && cudaMalloc(&p->scratch, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    plan_free(p);
+    return set_error(ARA_E_NOMEM, "metric scratch");
+  }
+  // one eager step first: builds the folds and caches every launch attribute, so the capture records
+  // stream work only (and validates the arguments)
+  st = plan_step(c, yet, ylt, rps, m, pml_dev, tvar_dev, p->scratch, bytes, s);
+  if (st == ARA_OK && cudaStreamSynchronize(s) != cudaSuccess) st = cuda_error(cudaGetLastError(), "plan warm-up");
+  cudaStream_t cs = nullptr;
+  if (st == ARA_OK && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+    st = cuda_error(cudaGetLastError(), "capture stream");
+  if (st == ARA_OK) {
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      st = cuda_error(e, "cudaStreamBeginCapture");
+    } else {
+      st = plan_step(c, yet, ylt, rps, m, pml_dev, tvar_dev, p->scratch, bytes, cs);
+      e = cudaStreamEndCapture(cs, &p->graph);
+      if (st == ARA_OK && e != cudaSuccess) st = cuda_error(e, "cudaStreamEndCapture");
+      if (st == ARA_OK && (e = cudaGraphInstantiate(&p->exec, p->graph, 0)) != cudaSuccess)
+        st = cuda_error(e, "cudaGraphInstantiate");
+    }
+  }
+  if (cs) cudaStreamDestroy(cs);
+  if (st) {
+    plan_free(p);
+    return st;
+  }
+  *out = p;
+  return ARA_OK;
+}
+
+ara_status ara_plan_launch(ara_plan* p, void* stream) {
+  if (!p || !p->exec) return set_error(ARA_E_ARG, "plan is NULL");
+  DeviceGuard guard(p->device);
+  ARA_CUDA(cudaGraphLaunch(p->exec, (cudaStream_t)stream));
+  return ARA_OK;
+}
+
+void ara_plan_destroy(ara_plan* p) { plan_free(p); }
 
 ara_status ara_check(ara_ctx* c, void* stream) {
   if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
@@ -983,6 +1090,10 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
       if (v < 0 || v > 1) return set_error(ARA_E_ARG, "precombined in {0, 1}");
       c->precombined = (int)v;
       return ARA_OK;
+    case ARA_OPT_TRIAL_ORDER:
+      if (v < 0 || v > 1) return set_error(ARA_E_ARG, "trial order in {0 blocks, 1 interleaved}");
+      c->interleave = (int)v;
+      return ARA_OK;
     case ARA_OPT_ROUND_MIN:
       if (v == 0) v = 24;
       if (v < 1 || v > 32) return set_error(ARA_E_ARG, "round trigger in [1, 32]");
@@ -1012,6 +1123,7 @@ ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
     case ARA_OPT_PRECOMBINED: *v = c->precombined; return ARA_OK;
     case ARA_OPT_STREAM: *v = c->stream_kernel; return ARA_OK;
     case ARA_OPT_ROUND_MIN: *v = c->round_min; return ARA_OK;
+    case ARA_OPT_TRIAL_ORDER: *v = c->interleave; return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }

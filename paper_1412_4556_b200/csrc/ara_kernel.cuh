@@ -51,6 +51,7 @@ struct LayerParams {
   const uint32_t* exact;     // UNFOLDED presence bitmap (bit e of word e >> 5), for the FX filter stage
   const double* occ;         // precombined occurrence-net loss FT2(sum_j FT1(l_ej)) per event
   uint32_t round_min;        // lane kernel: lanes with a queued hit that trigger a gather round
+  uint32_t interleave;       // fixed-length kernels: 1 = trials interleaved over the grid's warps, 0 = blocks
   double r1[kMaxJ], l1[kMaxJ];  // FT1 per table column (padding columns: 0, +inf)
 };
 

@@ -11,6 +11,11 @@ namespace ara {
 ara_status set_error(ara_status s, const char* fmt, ...);
 ara_status cuda_error(cudaError_t e, const char* what);
 
+// metrics.cu: PML/TVaR into caller-provided device scratch (no allocation, graph-capturable)
+size_t metrics_scratch_size(uint64_t n);
+ara_status metrics_device_into(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
+                               double* tvar_dev, char* scratch, size_t bytes, cudaStream_t s);
+
 // Restores the caller's current device on scope exit.
 struct DeviceGuard {
   int prev = -1;

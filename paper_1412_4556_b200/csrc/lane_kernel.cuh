@@ -65,8 +65,38 @@ __device__ __forceinline__ void test_enqueue(uint32_t id, uint32_t C, uint32_t f
       : "memory");
 }
 
+// XS (exact scan filter, for catalogues far larger than the shared bitmap, config X): the folded test
+// only nominates CANDIDATES; each candidate loads the word of the layer's unfolded presence bitmap
+// (global memory, L2-resident, bit e = row e holds a loss) that decides it exactly.  The load is issued
+// while scanning window w and used one window later, where only exact hits (and invalid ids, forced
+// through) enter the lane's queue.  A false positive then costs one L2 word instead of a queue slot, a
+// gather round and a record fetch; the queue order -- hence the YLT bits -- is unchanged.
+__device__ __forceinline__ uint32_t fold_candidate(uint32_t id, uint32_t C, uint32_t fmul, uint32_t bits_s,
+                                                   uint32_t valid, uint32_t& x) {
+  x = min(id - 1u, C);
+  const uint32_t w = lds_ro_u32(bits_s + 4u * __umulhi(x, fmul));
+  return (w >> (x & 31u)) & valid & 1u;
+}
+
+// Append x to the lane's queue when bit (x + 1) & 31 of the exact word is set.
+__device__ __forceinline__ void exact_enqueue(uint32_t ew, uint32_t x, uint32_t q_l, uint32_t& tail) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " .reg .b32 s, m, a;\n"
+      " add.u32 s, %1, 1;\n and.b32 s, s, 31;\n shl.b32 m, 1, s;\n and.b32 m, m, %2;\n setp.ne.b32 p, m, 0;\n"
+      " and.b32 a, %0, 0x380;\n or.b32 a, a, %3;\n"
+      " @p st.shared.u32 [a], %1;\n"
+      " @p add.u32 %0, %0, 128;\n"
+      "}\n"
+      : "+r"(tail)
+      : "r"(x), "r"(ew), "r"(q_l)
+      : "memory");
+}
+
 // NW: warps per block (one block per SM).  OLT: also the largest occurrence-net loss per trial.
-template <int NW, bool OLT>
+// XS: exact scan filter (see exact_enqueue).
+template <int NW, bool OLT, bool XS = false>
 __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_constant__ LayerParams p) {
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) uint32_t smem[];
@@ -79,20 +109,24 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = __shfl_sync(FULL, threadIdx.x >> 5, 0);  // warp-uniform for the compiler
   const uint32_t base_s = (uint32_t)__cvta_generic_to_shared(smem + t1_w + jpad * 4u);
-  const uint32_t wq_s = ((base_s + 1023u) & ~1023u) + warp * kLaneWarpSmem;  // 1 KB aligned queues
+  // all warps' queues first (1 KB each, so every queue is 1 KB aligned and an entry address is an OR),
+  // then the warps' record slots (512 B each)
+  const uint32_t wq_s = ((base_s + 1023u) & ~1023u) + warp * (32u * kLaneQ * 4u);
   uint32_t q_l;  // entry j of this lane's queue: q_l + 128 j (one register: the OR with the entry offset)
   asm volatile("mov.u32 %0, %1;" : "=r"(q_l) : "r"(wq_s + 4u * lane));
-  const uint32_t rec_l = wq_s + 32u * kLaneQ * 4u + 16u * lane;  // this lane's record slot
+  const uint32_t rec_l = ((base_s + 1023u) & ~1023u) + NW * (32u * kLaneQ * 4u) + warp * 512u + 16u * lane;
 
   for (uint32_t j = threadIdx.x; j < jpad; j += blockDim.x) s_t1[j] = make_double2(p.r1[j], p.l1[j]);
   for (uint32_t w = threadIdx.x; w < fw; w += blockDim.x) smem[w] = __ldg(p.present + w);
   __syncthreads();
 
-  // this warp's contiguous block of trials [t0, t0 + nt)
+  // this warp's trials t0 + k * tstep, k < nt: a contiguous block (tstep 1) or interleaved over the grid
   const uint64_t W = (uint64_t)blockIdx.x * NW + warp, NWT = (uint64_t)gridDim.x * NW;
   const uint64_t N = p.num_trials;
-  const uint64_t t0 = (uint64_t)(((unsigned __int128)W * N) / NWT);
-  const uint32_t nt = (uint32_t)((uint64_t)(((unsigned __int128)(W + 1) * N) / NWT) - t0);
+  const uint64_t tstep = p.interleave ? NWT : 1u;
+  const uint64_t t0 = p.interleave ? W : (uint64_t)(((unsigned __int128)W * N) / NWT);
+  const uint32_t nt = p.interleave ? (uint32_t)(N > W ? (N - 1 - W) / NWT + 1 : 0)
+                                   : (uint32_t)((uint64_t)(((unsigned __int128)(W + 1) * N) / NWT) - t0);
   if (nt == 0) return;  // warp-uniform
 
   const uint32_t K = p.K;                       // > 0, multiple of 4
@@ -102,6 +136,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
   const uint32_t C = p.C;
   const uint32_t fmul = p.fold_mul;
   const uint32_t round_min = p.round_min;       // lanes with a queued hit that trigger a round
+  const uint64_t pol_exact = make_policy(true, p.l2_hints);  // XS: the exact bitmap stays in L2
 
   // ---- per-lane queue state: tail/head count entries in units of 128 (the queue stride), so an
   // entry's address is q_l | (count & 0x380)
@@ -173,22 +208,49 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
     double Sv = par ? S1 : S0;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) Sv += __shfl_xor_sync(FULL, Sv, off);
-    if (lane == 0) p.ylt[t0 + kc] = clamp_terms(Sv, p.r3, p.l3);  // step 4: FT3 on S_n
+    if (lane == 0) p.ylt[t0 + (uint64_t)kc * tstep] = clamp_terms(Sv, p.r3, p.l3);  // step 4: FT3 on S_n
     if constexpr (OLT) {
       double M = par ? M1 : M0;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(FULL, M, off));
-      if (lane == 0) p.olt[t0 + kc] = M;
+      if (lane == 0) p.olt[t0 + (uint64_t)kc * tstep] = M;
       if (par) M1 = 0.0; else M0 = 0.0;
     }
     if (par) S1 = 0.0; else S0 = 0.0;
   };
   // Scan one window: presence test per id, hits appended to the lane's own queue.
+  // XS: the previous window's candidates (x, exact word; a non-candidate holds word 0)
+  uint32_t px0 = 0, px1 = 0, px2 = 0, px3 = 0, pw0 = 0, pw1 = 0, pw2 = 0, pw3 = 0;
+  auto exact_load = [&](uint32_t cand, uint32_t x) -> uint32_t {
+    uint32_t w = 0u;
+    if (cand) w = x < C ? ld_id(p.exact + ((x + 1u) >> 5), pol_exact) : 0xffffffffu;  // invalid: forced hit
+    return w;
+  };
+  auto flush_pending = [&]() {  // XS: the previous window's exact hits enter the queue (in slot order)
+    exact_enqueue(pw0, px0, q_l, tail);
+    exact_enqueue(pw1, px1, q_l, tail);
+    exact_enqueue(pw2, px2, q_l, tail);
+    exact_enqueue(pw3, px3, q_l, tail);
+    pw0 = pw1 = pw2 = pw3 = 0u;
+  };
   auto scan = [&](const uint4 v, uint32_t valid) {
-    test_enqueue(v.x, C, fmul, bits_s, valid, q_l, tail);
-    test_enqueue(v.y, C, fmul, bits_s, valid, q_l, tail);
-    test_enqueue(v.z, C, fmul, bits_s, valid, q_l, tail);
-    test_enqueue(v.w, C, fmul, bits_s, valid, q_l, tail);
+    if constexpr (XS) {
+      flush_pending();
+      uint32_t c;
+      c = fold_candidate(v.x, C, fmul, bits_s, valid, px0);
+      pw0 = exact_load(c, px0);
+      c = fold_candidate(v.y, C, fmul, bits_s, valid, px1);
+      pw1 = exact_load(c, px1);
+      c = fold_candidate(v.z, C, fmul, bits_s, valid, px2);
+      pw2 = exact_load(c, px2);
+      c = fold_candidate(v.w, C, fmul, bits_s, valid, px3);
+      pw3 = exact_load(c, px3);
+    } else {
+      test_enqueue(v.x, C, fmul, bits_s, valid, q_l, tail);
+      test_enqueue(v.y, C, fmul, bits_s, valid, q_l, tail);
+      test_enqueue(v.z, C, fmul, bits_s, valid, q_l, tail);
+      test_enqueue(v.w, C, fmul, bits_s, valid, q_l, tail);
+    }
     // rounds: enough lanes hold a hit, or a queue could overflow in the next window (<= 4 more; a queue
     // of 8 entries takes them while it holds <= 4)
     const uint32_t full = __ballot_sync(FULL, tail - head >= (kLaneQ - 3u) * 128u);
@@ -212,7 +274,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
     }
     pb = (tail - head) >> 7;
     curpar = k & 1u;
-    if (p.prefetch && lane == 0 && k + 2u < nt) prefetch_l2_bulk(lp + 2u * K - 4u * lane, K * 4u);
+    if (p.prefetch && lane == 0 && k + 2u < nt) prefetch_l2_bulk(lp + 2u * tstep * K - 4u * lane, K * 4u);
     // ---- the trial's windows (A holds the next one; pairs of full windows alternate A and B)
     const uint32_t* wp = lp;
     for (uint32_t i = 0; i < npair; ++i, wp += 256) {
@@ -226,10 +288,14 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
       scan(A, FULL);
       A = B;
     }
-    lp += K;
+    lp += tstep * K;
     if (k + 1u < nt && (nfull != 0u || lane_last)) B = ld_ids4_stream(lp);  // next trial's first window
     scan(A, last_valid);  // the tail window
     A = B;
+    if constexpr (XS) {  // the trial's last window: its exact hits before the trial boundary
+      flush_pending();
+      while (__any_sync(FULL, tail - head >= (kLaneQ - 3u) * 128u)) round();
+    }
   }
   // ---- drain every queue, then close the (at most two) open trials
   while (__any_sync(FULL, tail != head)) round();

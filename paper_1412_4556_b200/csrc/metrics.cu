@@ -441,27 +441,41 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
   }
 }
 
+// Per-device launch facts of the fused kernel, queried once (host-side cache; no per-call queries).
+struct FusedInfo {
+  int ready = 0, coop = 0, sms = 148, occ = 0;
+};
+static FusedInfo g_fused[64];
+
+static const FusedInfo& fused_info() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  FusedInfo& f = g_fused[dev & 63];
+  if (!f.ready) {
+    cudaDeviceGetAttribute(&f.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&f.coop, cudaDevAttrCooperativeLaunch, dev);
+    const size_t dyn = (size_t)kCacheKeys * sizeof(uint64_t);
+    cudaFuncSetAttribute((const void*)metrics_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f.occ, (const void*)metrics_fused, kFusedBlock, dyn) != cudaSuccess) {
+      cudaGetLastError();
+      f.occ = 0;
+    }
+    f.ready = 1;
+  }
+  return f;
+}
+
 // Launch the fused kernel cooperatively for one batch of <= kMaxQ queries, results to DEVICE pml/tvar
 // (either may be null); asynchronous.  Returns false if the device refuses a cooperative launch of the
 // needed size (callers fall back to the pass kernels).
 static bool metrics_fused_batch(const double* ylt, uint64_t n, int mq, const uint64_t* ks, char* scratch,
                                 size_t scratch_bytes, double* pml_dev, double* tvar_dev, cudaStream_t s,
                                 cudaError_t* err) {
-  int dev = 0, sms = 148, occ = 0;
   *err = cudaSuccess;
-  if (cudaGetDevice(&dev) != cudaSuccess) return false;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int coop = 0;
-  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  if (!coop) return false;
+  const FusedInfo& f = fused_info();
+  if (!f.coop || f.occ < 1) return false;
   const size_t dyn = (size_t)kCacheKeys * sizeof(uint64_t);
-  cudaFuncSetAttribute((const void*)metrics_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)metrics_fused, kFusedBlock, dyn) != cudaSuccess ||
-      occ < 1) {
-    cudaGetLastError();
-    return false;
-  }
-  uint64_t grid = (uint64_t)sms * occ;
+  uint64_t grid = (uint64_t)f.sms * f.occ;
   const uint64_t need = (n + kFusedBlock - 1) / kFusedBlock;
   if (grid > need) grid = need;
   const size_t state = sizeof(FusedState);
@@ -570,17 +584,15 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
   return rc;
 }
 
-// Asynchronous variant: results to DEVICE pml_dev[m] / tvar_dev[m]; needs cooperative launch.
-static ara_status metrics_device(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
-                                 double* tvar_dev, cudaStream_t s) {
+// Asynchronous variant into caller-provided device scratch (metrics_scratch_size(n) bytes): results to
+// DEVICE pml_dev[m] / tvar_dev[m]; needs cooperative launch.  No allocation, no synchronisation, so it
+// can be captured into a CUDA graph (ara_plan_create).
+ara_status metrics_device_into(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
+                               double* tvar_dev, char* scratch, size_t bytes, cudaStream_t s) {
   if (!ylt || (!pml_dev && !tvar_dev)) return set_error(ARA_E_ARG, "NULL argument");
   std::vector<uint64_t> ks;
   ara_status rc = ranks_for(n, rps, m, ks);
   if (rc) return rc;
-  uint64_t blocks = 0;
-  const size_t bytes = scratch_bytes(n, &blocks);
-  char* scratch = nullptr;
-  ARA_CUDA(cudaMallocAsync((void**)&scratch, bytes, s));
   for (uint32_t q0 = 0; q0 < m && rc == ARA_OK; q0 += kMaxQ) {
     const int mq = (int)std::min<uint32_t>(kMaxQ, m - q0);
     cudaError_t e = cudaSuccess;
@@ -590,6 +602,22 @@ static ara_status metrics_device(const double* ylt, uint64_t n, const double* rp
     else if (e != cudaSuccess)
       rc = cuda_error(e, "fused metric kernel");
   }
+  return rc;
+}
+
+size_t metrics_scratch_size(uint64_t n) {
+  uint64_t blocks = 0;
+  return scratch_bytes(n, &blocks);
+}
+
+// Asynchronous variant with its own stream-ordered scratch allocation.
+static ara_status metrics_device(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
+                                 double* tvar_dev, cudaStream_t s) {
+  if (!ylt || (!pml_dev && !tvar_dev)) return set_error(ARA_E_ARG, "NULL argument");
+  const size_t bytes = metrics_scratch_size(n);
+  char* scratch = nullptr;
+  ARA_CUDA(cudaMallocAsync((void**)&scratch, bytes, s));
+  ara_status rc = metrics_device_into(ylt, n, rps, m, pml_dev, tvar_dev, scratch, bytes, s);
   cudaFreeAsync(scratch, s);
   return rc;
 }

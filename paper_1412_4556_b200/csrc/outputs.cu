@@ -61,11 +61,16 @@ __global__ void __launch_bounds__(kOutBlock) ep_kernel(const double* __restrict_
     sx[i] = x[i];
   }
   __syncthreads();
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const double v = y[i];
+  // warp-uniform trip count (every lane of the warp iterates together), validity as a predicate, so the
+  // ballots always see the full warp and lane 0 counts
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const double v = valid ? y[i] : 0.0;
     for (int k = 0; k < m; ++k) {
-      const unsigned ball = __ballot_sync(__activemask(), v >= sx[k]);
-      if ((threadIdx.x & 31) == (unsigned)(__ffs(__activemask()) - 1) && ball) atomicAdd(&c[k], (unsigned long long)__popc(ball));
+      const unsigned ball = __ballot_sync(0xffffffffu, valid && v >= sx[k]);
+      if ((threadIdx.x & 31) == 0 && ball) atomicAdd(&c[k], (unsigned long long)__popc(ball));
     }
   }
   __syncthreads();

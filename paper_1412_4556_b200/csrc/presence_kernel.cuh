@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   __shared__ double2 s_t1[kCarry ? JPS : 1];  // record batches: FT1 as (R, L) pairs, one 16-B load per column
   __shared__ WarpTrials s_wt[NW];
   uint32_t* bits = smem;  // [present_words], already folded by the host (fold_mul)
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // provably warp-uniform for ptxas
   const int lane = threadIdx.x & 31;
   uint32_t* q = smem + p.present_words + warp * kQueue;
   WarpTrials& wt = s_wt[warp];
@@ -458,8 +458,8 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
     const int par = (int)(k & 1u);
     uint64_t b, e;
     if (p.offsets) {
-      b = p.offsets[t];
-      e = p.offsets[t + 1];
+      b = __shfl_sync(FULL, p.offsets[t], 0);  // warp-uniform (every lane loaded the same value)
+      e = __shfl_sync(FULL, p.offsets[t + 1], 0);
       if (e < b || e > p.num_events) {
         bad |= 2u;
         e = b;

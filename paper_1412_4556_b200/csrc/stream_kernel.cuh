@@ -96,12 +96,13 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_stream_kernel(const __grid_con
   for (uint32_t w = threadIdx.x; w < fw; w += blockDim.x) bits[w] = __ldg(p.present + w);
   __syncthreads();
 
-  // this warp's contiguous block of trials [t0, t0 + nt)
+  // this warp's trials t0 + k * tstep, k < nt: a contiguous block (tstep 1) or interleaved over the grid
   const uint64_t W = (uint64_t)blockIdx.x * NW + warp, NWT = (uint64_t)gridDim.x * NW;
   const uint64_t N = p.num_trials;
-  const uint64_t t0 = (uint64_t)(((unsigned __int128)W * N) / NWT);
-  const uint64_t t1 = (uint64_t)(((unsigned __int128)(W + 1) * N) / NWT);
-  const uint32_t nt = (uint32_t)(t1 - t0);
+  const uint64_t tstep = p.interleave ? NWT : 1u;
+  const uint64_t t0 = p.interleave ? W : (uint64_t)(((unsigned __int128)W * N) / NWT);
+  const uint32_t nt = p.interleave ? (uint32_t)(N > W ? (N - 1 - W) / NWT + 1 : 0)
+                                   : (uint32_t)((uint64_t)(((unsigned __int128)(W + 1) * N) / NWT) - t0);
   if (nt == 0) return;  // warp-uniform
 
   const uint32_t K = p.K;                       // > 0, multiple of 4
@@ -133,12 +134,12 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_stream_kernel(const __grid_con
     double Sr = __shfl_sync(FULL, S, (lane + fO) & 31u);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) Sr += __shfl_xor_sync(FULL, Sr, off);
-    if (lane == 0) p.ylt[t0 + kO] = clamp_terms(Sr, p.r3, p.l3);  // step 4: FT3 on S_n
+    if (lane == 0) p.ylt[t0 + (uint64_t)kO * tstep] = clamp_terms(Sr, p.r3, p.l3);  // step 4: FT3 on S_n
     if constexpr (OLT) {
       double M = Mx;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) M = fmax(M, __shfl_xor_sync(FULL, M, off));
-      if (lane == 0) p.olt[t0 + kO] = M;
+      if (lane == 0) p.olt[t0 + (uint64_t)kO * tstep] = M;
       Mx = 0.0;
     }
     S = 0.0;
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_stream_kernel(const __grid_con
     if (k == kO + 1u) nb = qt >> 2;
     if (k == kO) fO = qt >> 2;
     kcur = k;
-    if (p.prefetch && lane == 0 && k + 2u < nt) prefetch_l2_bulk(lp + 2u * K - 4u * lane, K * 4u);
+    if (p.prefetch && lane == 0 && k + 2u < nt) prefetch_l2_bulk(lp + 2u * tstep * K - 4u * lane, K * 4u);
     const uint32_t* wp = lp;
     for (uint32_t i = 0; i < npair; ++i, wp += 256) {  // full windows 2i (in A) and 2i+1
       B = ld_ids4_stream(wp + 128);                    // window 2i+1 < nfull: full
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_stream_kernel(const __grid_con
       wp += 128;
     }
     // the tail window (in A); its successor is the next trial's first window
-    lp += K;
+    lp += tstep * K;
     if (k + 1u < nt && (nfull != 0u || lane_last)) B = ld_ids4_stream(lp);
     scan(A, last_valid);
     A = B;

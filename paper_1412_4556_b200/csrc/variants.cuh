@@ -36,6 +36,7 @@ struct StreamVariant {
   KernelFn fn, fn_olt;
   const char* name;
   int ring;  // 0: per-lane queues (lane_kernel.cuh), 1: warp hit ring (stream_kernel.cuh)
+  int xs;    // 1: exact scan filter (lane_kernel.cuh XS)
 };
 const StreamVariant* stream_variants(int* n);  // kernels_stream.cu; first = default
 

@@ -46,30 +46,60 @@ def unshard_plan(starts: Sequence[int], cap: int, num_layers: int):
     return plan
 
 
+class YltGather:
+    """All-gather of per-rank YLT shards into the full [layers][N] YLT, with every buffer allocated once
+    (the step itself allocates nothing): ara_run writes straight into the padded send buffer when the
+    shard fills it, one NCCL all_gather_into_tensor, then ara_unshard (device memcpy2D) drops the
+    padding.  `local` is the [layers][shard] view a rank's ara_run should write into."""
+
+    def __init__(self, num_layers: int, num_trials: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.N = num_trials
+        self.L = num_layers
+        self.starts = shard_starts(num_trials, self.world)
+        self.cap = shard_cap(num_trials, self.world)
+        self.n_local = self.starts[self.rank + 1] - self.starts[self.rank]
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.send = torch.zeros((num_layers, self.cap), dtype=torch.float64, device=device)
+        self.recv = torch.empty((self.world, num_layers, self.cap), dtype=torch.float64, device=device)
+        self.full = torch.empty((num_layers, num_trials), dtype=torch.float64, device=device)
+        # ara_run's output: the send buffer itself when one layer fills it exactly, else a separate tensor
+        direct = num_layers == 1 or self.n_local == self.cap
+        self.local = self.send[:, :self.n_local] if (direct and num_layers == 1) else (
+            self.send if direct else torch.empty((num_layers, self.n_local), dtype=torch.float64, device=device))
+        self._host = None if self.nccl else torch.empty(self.world * num_layers * self.cap, dtype=torch.float64)
+
+    def gather(self, stream=None):
+        """Assemble self.full from every rank's self.local (stream-ordered; no allocation)."""
+        import torch.distributed as dist
+
+        from . import ara
+        if self.local.data_ptr() != self.send.data_ptr():
+            self.send[:, :self.n_local].copy_(self.local)  # pad the send rows (multi-layer, ragged shards)
+        if self.nccl:
+            dist.all_gather_into_tensor(self.recv.view(-1), self.send.view(-1), group=self.group)
+        else:  # gloo (several ranks sharing one GPU in tests): the same gather through host memory
+            dist.all_gather_into_tensor(self._host, self.send.view(-1).cpu(), group=self.group)
+            self.recv.view(-1).copy_(self._host)
+        ara.ara_unshard(self.recv, self.world, self.cap, self.L, self.starts, self.full, stream=stream)
+        return self.full
+
+
+_GATHERERS = {}
+
+
 def gather_ylt(local_ylt, num_trials: int, group=None):
     """All-gather per-rank YLT shards ([layers][shard] CUDA float64) into the full [layers][N] YLT on
-    every rank.  One NCCL all_gather_into_tensor plus ara_unshard."""
-    import torch
-    import torch.distributed as dist
-
-    from . import ara
-
-    world = dist.get_world_size(group)
-    L = local_ylt.shape[0]
-    starts = shard_starts(num_trials, world)
-    cap = shard_cap(num_trials, world)
-    if local_ylt.shape[1] == cap and local_ylt.is_contiguous():
-        send = local_ylt
-    else:
-        send = torch.empty((L, cap), dtype=local_ylt.dtype, device=local_ylt.device)
-        send[:, :local_ylt.shape[1]].copy_(local_ylt)  # plumbing: pad the send buffer (D2D copy)
-    recv = torch.empty((world, L, cap), dtype=local_ylt.dtype, device=local_ylt.device)
-    if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(recv.view(-1), send.reshape(-1), group=group)
-    else:  # gloo (testing several ranks on one GPU): the same gather through host memory
-        host = torch.empty(world * L * cap, dtype=local_ylt.dtype)
-        dist.all_gather_into_tensor(host, send.reshape(-1).cpu(), group=group)
-        recv.view(-1).copy_(host)
-    full = torch.empty((L, num_trials), dtype=local_ylt.dtype, device=local_ylt.device)
-    ara.ara_unshard(recv, world, cap, L, starts, full)
-    return full
+    every rank: one NCCL all_gather_into_tensor plus ara_unshard, through a cached YltGather (buffers
+    allocated on the first call for a given shape)."""
+    key = (local_ylt.shape[0], num_trials, local_ylt.device, id(group))
+    g = _GATHERERS.get(key)
+    if g is None:
+        g = _GATHERERS[key] = YltGather(local_ylt.shape[0], num_trials, local_ylt.device, group)
+    if local_ylt.data_ptr() != g.local.data_ptr():
+        g.local.copy_(local_ylt) if g.local.shape == local_ylt.shape else g.send[:, :local_ylt.shape[1]].copy_(local_ylt)
+    return g.gather()

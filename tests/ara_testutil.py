@@ -81,7 +81,7 @@ def within_tol(gpu, ref, rel=1e-6, abs_floor=1e-3):
 
 
 KERNEL_STREAM = 2       # test-level selector: the presence path with the fixed-length stream kernel
-STREAM_VARIANTS = 4     # ARA_OPT_STREAM = 1..4 (lane kernel 32, 24, 16 warps per block; ring kernel)
+STREAM_VARIANTS = 7     # ARA_OPT_STREAM = 1..7 (lane kernel 32/24/16 warps; ring kernel; lane XS 24/32/16)
 
 
 def select(ctx, kernel, variant=0):
@@ -92,9 +92,11 @@ def select(ctx, kernel, variant=0):
     if kernel == KERNEL_STREAM:
         ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
         ctx.ara_set_option(ara.ARA_OPT_STREAM, variant + 1)
+        ctx.ara_set_option(ara.ARA_OPT_FILTER, -1)
         return
     ctx.ara_set_option(ara.ARA_OPT_KERNEL, kernel)
-    ctx.ara_set_option(ara.ARA_OPT_STREAM, 1 if kernel == ara.KERNEL_AUTO else 0)
+    ctx.ara_set_option(ara.ARA_OPT_STREAM, 0)
+    ctx.ara_set_option(ara.ARA_OPT_FILTER, -1 if kernel == ara.KERNEL_AUTO else 0)
     if kernel != ara.KERNEL_AUTO:
         ctx.ara_set_option(ara.ARA_OPT_VARIANT, variant)
 

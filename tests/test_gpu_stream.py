@@ -113,9 +113,9 @@ def test_stream_sharding_invariant_and_vs_oracle(cuda_device):
     N, K = 12_000, cfg.kmin
     ids = synth.yet_ids(cfg.seed, cfg.catalog_size, 0, N * K)
     ctx = ara.context_for_config(cfg, elts)
-    select(ctx, ara.KERNEL_AUTO)
+    select(ctx, KERNEL_STREAM, 0)
     whole = gpu_ylt(None, ctx, ids, K=K, num_trials=N)
-    assert ctx.ara_kernel_name().startswith("ara_lane_kernel")  # the default for fixed-length trials
+    assert ctx.ara_kernel_name().startswith("ara_lane_kernel")
     for G in (2, 3, 8):
         starts = [(g * N) // G for g in range(G + 1)]
         parts = [gpu_ylt(None, ctx, ids[starts[g] * K:starts[g + 1] * K], K=K, num_trials=starts[g + 1] - starts[g])
@@ -149,3 +149,104 @@ def test_stream_olt_and_invalid_ids(cuda_device):
         assert e.value.status == ara.ARA_E_RANGE
         # a valid run afterwards is clean again
         assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N), wy)
+
+
+def test_plan_replays_eager_step_bitwise(cuda_device):
+    """ara_plan: the captured step (ara_run + PML/TVaR of every layer) replayed as a CUDA graph gives the
+    eager calls' YLT and metrics bit for bit, replay after replay; multi-layer, fixed-length YET."""
+    C, J, K, N = 20_000, 16, 1000, 3000
+    elts, layer, yet = _problem(J, C, 800, K, N, integer=False, seed=11)
+    layers = [layer, (list(range(8)), (100.0, 5e6), (1e4, 3e6))]
+    ctx = _ctx(C, elts, layers)
+    ids = torch.from_numpy(yet.view(np.int32)).cuda()
+    rps = synth.return_periods(N)
+    m = len(rps)
+    y_e = torch.zeros((2, N), dtype=torch.float64, device=cuda_device)
+    ctx.ara_run(ids, y_e, events_per_trial=K, num_trials=N)
+    ctx.ara_check()
+    want_p = [ara.ara_pml_tvar(y_e[l], rps) for l in range(2)]
+    y = torch.full((2, N), -1.0, dtype=torch.float64, device=cuda_device)
+    pml = torch.zeros((2, m), dtype=torch.float64, device=cuda_device)
+    tvar = torch.zeros((2, m), dtype=torch.float64, device=cuda_device)
+    plan = ctx.ara_plan_create(ids, y, rps, pml, tvar, events_per_trial=K, num_trials=N)
+    for _ in range(3):
+        y.fill_(-1.0)
+        pml.zero_()
+        plan.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_e)
+        for l in range(2):
+            assert np.array_equal(pml[l].cpu().numpy(), want_p[l][0]) and np.array_equal(tvar[l].cpu().numpy(), want_p[l][1])
+    ctx.ara_check()
+    want = oracle.ylt(C, yet, None, N, K, elts, layers)
+    assert np.all(within_tol(y.cpu().numpy(), want))
+    plan.close()
+
+
+def _sparse_problem(J, C, n, K, N, seed, integer=True):
+    """ELTs of n distinct ids each over a large catalogue (drawn without materialising it)."""
+    rng = np.random.default_rng(seed)
+    elts = []
+    for j in range(J):
+        ids = np.unique(rng.integers(1, C + 1, size=2 * n))[:n]
+        rng.shuffle(ids)
+        losses = (rng.integers(1, 1 << 20, size=ids.size) if integer else rng.random(ids.size) * 1e6 + 0.5)
+        elts.append((ids.astype(np.uint32), losses.astype(np.float32),
+                     (float(rng.integers(0, 1 << 16)), INF if j % 3 == 1 else float(rng.integers(1 << 18, 1 << 21)))))
+    yet = rng.integers(1, C + 1, size=N * K).astype(np.uint32)
+    layer = (list(range(J)), (5000.0, float(1 << 24)), (2e5, 4e7))
+    return elts, layer, yet
+
+
+def test_exact_scan_filter_stress_shape(cuda_device):
+    """Config X's shape (J = 100 ELTs of 10,000 entries over a 10M-event catalogue: the shared bitmap is
+    folded ~6.6x, ~48% of occurrences are candidates, ~80% of them false positives).  The lane kernel
+    with the exact scan filter (chosen automatically) equals the oracle bitwise (integer regime) for
+    every XS variant, also with the occurrence loss table, and the plain lane / presence kernels."""
+    C, J, n, K, N = 10_000_000, 100, 10_000, 1000, 1500
+    elts, layer, yet = _sparse_problem(J, C, n, K, N, seed=17)
+    wy, wo = oracle.ylt_olt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx(C, elts, [layer])
+    select(ctx, ara.KERNEL_AUTO)
+    got = gpu_ylt(None, ctx, yet, K=K, num_trials=N)
+    assert ctx.ara_kernel_name().endswith(",XS>"), ctx.ara_kernel_name()
+    assert np.array_equal(got, wy)
+    for v in (4, 5, 6, 0):  # XS 24/32/16 warps, plain lane kernel
+        assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=v), wy), v
+    assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=ara.KERNEL_PRESENCE, variant=0), wy)
+    select(ctx, ara.KERNEL_AUTO)
+    ids = torch.from_numpy(yet.view(np.int32)).cuda()
+    y = torch.zeros((1, N), dtype=torch.float64, device=cuda_device)
+    o = torch.full((1, N), -1.0, dtype=torch.float64, device=cuda_device)
+    ctx.ara_run_ex(ids, y, o, events_per_trial=K, num_trials=N)
+    ctx.ara_check()
+    assert np.array_equal(y.cpu().numpy(), wy) and np.array_equal(o.cpu().numpy(), wo)
+    # invalid ids are still reported through the exact filter
+    b = yet.copy()
+    b[K * 7 + 3] = C + 5
+    with pytest.raises(ara.AraError):
+        gpu_ylt(None, ctx, b, K=K, num_trials=N)
+
+
+def test_exact_scan_filter_config_x_sampled(cuda_device):
+    """Config X itself (real regime) on a 20,000-trial slice generated on the device: the automatic
+    kernel (lane + exact scan filter) within tolerance of the oracle on 500 sampled trials, and within
+    1e-12 relative of the presence kernel on every trial."""
+    cfg = synth.Config.load("X")
+    elts = synth.make_elts(cfg)
+    N, K = 20_000, cfg.kmin
+    ids = torch.empty(N * K, dtype=torch.int32, device=cuda_device)
+    synth.yet_ids_device(ids.data_ptr(), cfg.seed, cfg.catalog_size, 0, N * K, torch.cuda.current_stream().cuda_stream)
+    ctx = ara.context_for_config(cfg, elts)
+    y = torch.zeros((1, N), dtype=torch.float64, device=cuda_device)
+    ctx.ara_run(ids, y, events_per_trial=K, num_trials=N)
+    ctx.ara_check()
+    assert ctx.ara_kernel_name().endswith(",XS>"), ctx.ara_kernel_name()
+    got = y.cpu().numpy()
+    select(ctx, ara.KERNEL_PRESENCE, 0)
+    ctx.ara_run(ids, y, events_per_trial=K, num_trials=N)
+    ctx.ara_check()
+    assert np.all(within_tol(got, y.cpu().numpy(), rel=1e-12, abs_floor=1e-6))
+    sample = np.arange(0, N, 40)
+    want = oracle.ylt_for(cfg, elts, synth.make_yet_trials(cfg, sample))
+    assert np.all(within_tol(got[:, sample], want))
