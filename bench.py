@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--prefetch", type=int, default=None, choices=[-1, 0, 1], help="ARA_OPT_PREFETCH")
     ap.add_argument("--round-min", type=int, default=None, help="ARA_OPT_ROUND_MIN (lane kernel round trigger)")
     ap.add_argument("--trial-order", type=int, default=None, choices=[0, 1], help="ARA_OPT_TRIAL_ORDER")
+    ap.add_argument("--fused", type=int, default=None, choices=[0, 1], help="ARA_OPT_FUSED (multi-layer single pass)")
     ap.add_argument("--eager", action="store_true", help="issue the step's calls one by one (no captured plan)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -287,6 +288,8 @@ def main():
         ctx.ara_set_option(ara.ARA_OPT_ROUND_MIN, args.round_min)
     if args.trial_order is not None:
         ctx.ara_set_option(ara.ARA_OPT_TRIAL_ORDER, args.trial_order)
+    if args.fused is not None:
+        ctx.ara_set_option(ara.ARA_OPT_FUSED, args.fused)
     info = [ctx.ara_layer_info(l) for l in range(L)]
 
     # ---- this rank's YET shard, generated in HBM
@@ -495,7 +498,16 @@ def main():
     comp_bytes = float(np.mean([4.0 * occ + 8.0 * n_local + pr * rb + (cfg.catalog_size + 1) / 8.0
                                 for pr, rb in zip(present_rows, row_bytes)]))
     dense_bytes = float(np.mean([occ * (4 + rb) for rb in row_bytes]))  # 4 B id + row sectors
-    if sparse_path:
+    if kernel_name == "ara_fused_kernel":
+        # one launch streams the YET once for every layer: YET ids + every layer's YLT row, present rows
+        # and bitmap
+        launch_ms = kern_ms
+        alg_bytes_launch = 4.0 * occ + sum(8.0 * n_local + pr * rb + (cfg.catalog_size + 1) / 8.0
+                                           for pr, rb in zip(present_rows, row_bytes))
+        alg_note = ("fused multi-layer pass (one launch for %d layers): algorithmic bytes = compulsory HBM traffic: "
+                    "4 B YET id per occurrence once + per layer 8 B YLT per trial, its rows holding a loss and its "
+                    "presence bitmap (DESIGN.md 'Roofline')" % L)
+    elif sparse_path:
         alg_bytes_launch = comp_bytes
         alg_note = ("algorithmic bytes = compulsory HBM traffic: 4 B YET id per occurrence + 8 B YLT per trial + "
                     "one read of each table row holding a loss (%d rows x %d B) + the presence bitmap; rows of "
@@ -534,6 +546,49 @@ def main():
                  "note": "SURVEY.md 8(d) definition: occurrences x (4 B id + sector-rounded row); table gathers are "
                          "served mostly from DRAM (ncu: L2 hit ~36%)"}
         ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_AUTO)
+        ctx.ara_check(stream)
+    # ---- the layer-outer passes (Algorithm 1's loop order), timed beside the fused pass
+    outer_leg = None
+    if not args.profile and L > 1 and kernel_name == "ara_fused_kernel":
+        ref_ylt = ylt_local.clone()
+        ctx.ara_set_option(ara.ARA_OPT_FUSED, 0)
+        for _ in range(2):
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(3):
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        diff = (ylt_local - ref_ylt).abs()
+        over = diff > torch.maximum(1e-12 * ref_ylt.abs(), torch.full_like(ref_ylt, 1e-6))
+        rel = float((diff / ref_ylt.abs().clamp_min(1e-300))[ref_ylt.abs() > 1e-3].max()) if bool((ref_ylt.abs() > 1e-3).any()) else 0.0
+        first_bad = torch.nonzero(over)[:3].tolist()
+        outer_leg = {"kernel": ctx.ara_kernel_name(), "ms_all_layers": a.elapsed_time(b) / 3,
+                     "fused_ms_all_layers": kern_ms, "max_rel_diff_vs_fused": rel,
+                     "elements_beyond_1e-12": int(over.sum()), "first": first_bad,
+                     "first_values": [[float(ref_ylt[i, j]), float(ylt_local[i, j])] for i, j in first_bad],
+                     "note": "one pass per layer (PAPER.md:104-105) vs one fused pass over the YET (SURVEY.md N1)"}
+        ctx.ara_set_option(ara.ARA_OPT_FUSED, 1)
+        ctx.ara_check(stream)
+    elif not args.profile and L > 1 and cfg.fixed_length:  # the product is layer-outer: time the fused pass
+        ref_ylt = ylt_local.clone()
+        ctx.ara_set_option(ara.ARA_OPT_FUSED, 1)
+        for _ in range(2):
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(3):
+            ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        diff = (ylt_local - ref_ylt).abs()
+        over = diff > torch.maximum(1e-12 * ref_ylt.abs(), torch.full_like(ref_ylt, 1e-6))
+        outer_leg = {"kernel": ctx.ara_kernel_name(), "fused_ms_all_layers": a.elapsed_time(b) / 3,
+                     "layer_outer_ms_all_layers": kern_ms, "elements_beyond_1e-12_vs_layer_outer": int(over.sum()),
+                     "note": "SURVEY.md N1: one fused pass over the YET for all layers (ARA_OPT_FUSED=1) vs the "
+                             "layer-outer product path (PAPER.md:104-105); the fused pass is the slower one here"}
+        ctx.ara_set_option(ara.ARA_OPT_FUSED, 0)
         ctx.ara_check(stream)
     # ---- SURVEY N3 ablation: the precombined occurrence-net table o[e] (no ELT lookups at run time),
     # timed beside; its YLT must equal the product path's bit for bit (checked here)
@@ -602,6 +657,7 @@ def main():
                      "note": alg_note + f"; peak {peak_src}"},
         "dense_kernel": dense,
         "presence_kernel": presence_leg,
+        "layer_outer_N1": outer_leg,
         "precombined_N3": pre,
         "cpu_baseline": cpu,
         "e2e": e2e,

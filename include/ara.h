@@ -257,6 +257,13 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *   ARA_OPT_TRIAL_ORDER     fixed-length-trial kernels: 1 (default) trials interleaved over the grid's
  *                           warps (warp w takes trials w, w + W, ...: all warps stream one compact
  *                           region of the YET), 0 contiguous trial blocks per warp.  Same YLT bits.
+ *   ARA_OPT_FUSED           0 (default) layer-outer passes; 1: a run over several layers streams a fixed-length YET ONCE per
+ *                           group of consecutive sparse-path layers (<= 16 layers, <= 256 ELT columns;
+ *                           SURVEY.md N1; fused_kernel.cuh: union presence bitmap, combined per-event
+ *                           records, per-layer accumulators) instead of Algorithm 1's layer-outer loop
+ *                           (PAPER.md:104-105).  Measured slower on config M (N1), hence off.
+ *                           Not used for the occurrence loss table (ara_run_ex
+ *                           with olt), ragged YETs, or when ARA_OPT_STREAM / ARA_OPT_KERNEL select a kernel.
  * ARA_OPT_BLOCK_THREADS applies to the dense kernel; the presence kernel fixes its block size. */
 typedef enum {
   ARA_OPT_BLOCK_THREADS = 1,
@@ -269,7 +276,8 @@ typedef enum {
   ARA_OPT_PRECOMBINED = 8,
   ARA_OPT_STREAM = 9,
   ARA_OPT_ROUND_MIN = 10,
-  ARA_OPT_TRIAL_ORDER = 11
+  ARA_OPT_TRIAL_ORDER = 11,
+  ARA_OPT_FUSED = 12
 } ara_option;
 ARA_API ara_status ara_set_option(ara_ctx* ctx, ara_option opt, int64_t value);
 ARA_API ara_status ara_get_option(ara_ctx* ctx, ara_option opt, int64_t* value);

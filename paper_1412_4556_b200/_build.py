@@ -23,7 +23,7 @@ LIBS = {
     "libara_synth.so": [os.path.join(HERE, "synth", "synth.cu")],
 }
 DEPS = {
-    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_kernel.cuh", "presence_kernel.cuh", "stream_kernel.cuh", "lane_kernel.cuh", "variants.cuh", "study.cuh", "common.cuh")] + [os.path.join(INCLUDE, "ara.h")],
+    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_kernel.cuh", "presence_kernel.cuh", "stream_kernel.cuh", "lane_kernel.cuh", "fused_kernel.cuh", "variants.cuh", "study.cuh", "common.cuh")] + [os.path.join(INCLUDE, "ara.h")],
     "libara_synth.so": [os.path.join(INCLUDE, "ara_synth.h")],
 }
 OUT_DIR = {"libara.so": HERE, "libara_synth.so": os.path.join(HERE, "synth")}

@@ -28,6 +28,7 @@ ARA_OPT_PRECOMBINED = 8
 ARA_OPT_STREAM = 9
 ARA_OPT_ROUND_MIN = 10
 ARA_OPT_TRIAL_ORDER = 11
+ARA_OPT_FUSED = 12
 KERNEL_AUTO, KERNEL_PRESENCE, KERNEL_DENSE = -1, 0, 1
 STUDY_INTERLEAVED, STUDY_INDEPENDENT, STUDY_SORTED = 0, 1, 2
 ARA_MAX_ELTS_PER_LAYER = 128

@@ -17,6 +17,7 @@
 #include "presence_kernel.cuh"
 #include "stream_kernel.cuh"
 #include "lane_kernel.cuh"
+#include "fused_kernel.cuh"
 #include "variants.cuh"
 #include "study.cuh"
 #include "common.cuh"
@@ -116,6 +117,15 @@ struct ara_ctx {
   int precombined = 0;  // ARA_OPT_PRECOMBINED: 1 = gather o[e] from the precombined table
   int variant = 0;
   int kernel = -1;  // KernelKind, or -1 = per-layer automatic choice
+  int fused = 0;          // ARA_OPT_FUSED: 1 one pass over the YET per layer group, 0 layer-outer (default: measured faster on M)
+  struct FusedGroup {       // layers [l0, l1) fused into one pass (fused_kernel.cuh)
+    uint32_t l0 = 0, l1 = 0, cols = 0;
+    uint4* rec = nullptr;           // (C + 2) x 32 B combined records
+    uint32_t* present = nullptr;    // union presence bitmap
+    std::vector<ara::Layer::Fold> folds;
+  };
+  std::vector<FusedGroup> groups;  // built on the first fused run
+  bool groups_built = false;
   int interleave = 1;     // ARA_OPT_TRIAL_ORDER: 1 trials interleaved over the warps, 0 contiguous blocks
   int round_min = 24;     // ARA_OPT_ROUND_MIN: lane kernel round trigger (lanes holding a queued hit)
   int stream_kernel = 0;  // ARA_OPT_STREAM: 0 off, v > 0 = stream variant v - 1 for fixed-length trials
@@ -244,6 +254,45 @@ __global__ void __launch_bounds__(256) record_build_kernel(uint4* __restrict__ r
   }
 }
 
+// the union presence bitmap of a layer group (word-wise OR of the layers' bitmaps).
+__global__ void __launch_bounds__(256) union_bitmap_kernel(uint32_t* __restrict__ out, const uint32_t* const* in,
+                                                           uint32_t nl, uint32_t words) {
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < words; w += gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    for (uint32_t l = 0; l < nl; ++l) v |= in[l][w];
+    out[w] = v;
+  }
+}
+
+struct FusedBuildArgs {
+  const float* table[kFusedMaxLayers];
+  uint32_t jpad[kFusedMaxLayers], J[kFusedMaxLayers], col0[kFusedMaxLayers];
+  uint32_t nl;
+};
+
+// combined 32-B record per event over a layer group: up to four (global column, loss) entries
+// in layer/column order, their count (more than four: read the layer rows in full), the event id.
+__global__ void __launch_bounds__(256) fused_record_kernel(uint4* __restrict__ rec, const __grid_constant__ FusedBuildArgs a,
+                                                           uint64_t rows) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t n = 0, cols = 0, l[4] = {0u, 0u, 0u, 0u};
+    for (uint32_t ly = 0; ly < a.nl; ++ly) {
+      const float* row = a.table[ly] + e * a.jpad[ly];
+      for (uint32_t j = 0; j < a.J[ly]; ++j) {
+        const uint32_t b = __float_as_uint(row[j]);
+        if (b == 0u) continue;
+        if (n < 4u) {
+          cols |= (a.col0[ly] + j) << (8u * n);
+          l[n] = b;
+        }
+        ++n;
+      }
+    }
+    rec[2 * e] = make_uint4(cols, n, l[0], l[1]);
+    rec[2 * e + 1] = make_uint4(l[2], l[3], (uint32_t)e, 0u);
+  }
+}
+
 // o[e] = FT2(sum_j FT1(T[e][j])) per event, summed over the layer's columns in order with the
 // kernels' clamp (absent losses give exact +0 terms), so it equals the record path's value bit for bit.
 __global__ void __launch_bounds__(256) occ_build_kernel(double* __restrict__ occ, const float* __restrict__ table,
@@ -274,6 +323,11 @@ static void destroy_ctx(ara_ctx* c) {
     cudaFree(L.sorted_ids);
     cudaFree(L.sorted_loss);
     cudaFree(L.sorted_off);
+  }
+  for (auto& g : c->groups) {
+    cudaFree(g.rec);
+    cudaFree(g.present);
+    for (auto& f : g.folds) cudaFree(f.buf);
   }
   cudaFree(c->d_err);
   cudaFreeHost(c->h_err);
@@ -515,8 +569,170 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   return ARA_OK;
 }
 
+// consecutive presence layers grouped for the fused kernel (<= 16 layers, <= 256 columns).
+static ara_status build_groups(ara_ctx* c, cudaStream_t s) {
+  c->groups_built = true;
+  const uint32_t nlay = (uint32_t)c->layers.size();
+  const uint64_t rows = (uint64_t)c->C + 1;
+  uint32_t l = 0;
+  while (l < nlay) {
+    ara_ctx::FusedGroup g;
+    g.l0 = l;
+    uint32_t cols = 0;
+    while (l < nlay && l - g.l0 < (uint32_t)kFusedMaxLayers && cols + c->layers[l].J <= (uint32_t)kFusedMaxCols) {
+      cols += c->layers[l].J;
+      ++l;
+    }
+    if (l == g.l0) ++l;  // a single layer wider than 256 columns: runs on its own
+    g.l1 = l;
+    g.cols = cols;
+    c->groups.push_back(g);
+  }
+  for (auto& g : c->groups) {
+    const uint32_t nl = g.l1 - g.l0;
+    if (nl < 2) continue;
+    const uint32_t words = c->layers[0].present_words;
+    if (cudaMalloc(&g.rec, (rows + 1) * 32) != cudaSuccess || cudaMalloc(&g.present, (size_t)words * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return set_error(ARA_E_NOMEM, "fused layer-group records");
+    }
+    ARA_CUDA(cudaMemsetAsync(g.rec + 2 * rows, 0, 32, s));  // record C + 1: all zero (invalid ids)
+    const uint32_t* h_in[kFusedMaxLayers];
+    FusedBuildArgs a;
+    memset(&a, 0, sizeof a);
+    a.nl = nl;
+    uint32_t col = 0;
+    for (uint32_t i = 0; i < nl; ++i) {
+      const Layer& L = c->layers[g.l0 + i];
+      h_in[i] = L.present;
+      a.table[i] = L.table;
+      a.jpad[i] = L.jpad;
+      a.J[i] = L.J;
+      a.col0[i] = col;
+      col += L.J;
+    }
+    const uint32_t** d_in = nullptr;
+    ARA_CUDA(cudaMalloc(&d_in, sizeof h_in));
+    ARA_CUDA(cudaMemcpyAsync(d_in, h_in, sizeof h_in, cudaMemcpyHostToDevice, s));
+    const unsigned ub = (unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)c->sms * 8);
+    union_bitmap_kernel<<<ub, 256, 0, s>>>(g.present, d_in, nl, words);
+    ARA_CUDA(cudaGetLastError());
+    const unsigned rb = (unsigned)std::min<uint64_t>((rows + 255) / 256, (uint64_t)c->sms * 16);
+    fused_record_kernel<<<rb, 256, 0, s>>>(g.rec, a, rows);
+    ARA_CUDA(cudaGetLastError());
+    ARA_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_in);
+  }
+  return ARA_OK;
+}
+
+static ara_status launch_fused(ara_ctx* c, ara_ctx::FusedGroup& g, const uint32_t* ids, uint64_t num_trials,
+                               uint64_t num_events, uint32_t K, double* ylt, uint64_t ld, cudaStream_t stream) {
+  constexpr int NW = 16;
+  const uint32_t nl = g.l1 - g.l0;
+  const void* fn = (const void*)ara_fused_kernel<NW>;
+  int st_smem = 0;
+  ara_status st = fn_static_smem(c, fn, &st_smem);
+  if (st) return st;
+  const int64_t budget = (int64_t)c->smem_optin - st_smem - (int64_t)fused_smem_extra(NW, nl);
+  if (budget < 4096) return set_error(ARA_E_UNSUPPORTED, "no shared memory left for the fused bitmap");
+  // fold the union bitmap (the folds of the group are cached like a layer's)
+  const Layer& L0 = c->layers[g.l0];
+  const uint64_t C = c->C;
+  const uint32_t fw = (uint32_t)std::min<int64_t>(L0.present_words, budget / 4);
+  const uint32_t mul = (C + 1 <= 32ull * fw) ? (1u << 27) : (uint32_t)((((uint64_t)fw << 32) - 1) / C);
+  const uint32_t* fold = nullptr;
+  for (auto& f : g.folds)
+    if (f.words == fw && f.mul == mul) fold = f.buf;
+  if (!fold) {
+    uint32_t* b = nullptr;
+    if (cudaMalloc(&b, (size_t)fw * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return set_error(ARA_E_NOMEM, "folded union bitmap");
+    }
+    ARA_CUDA(cudaMemsetAsync(b, 0, (size_t)fw * 4, stream));
+    const unsigned fb = (unsigned)std::min<uint64_t>((L0.present_words + 255) / 256, 4096);
+    presence_fold_kernel<<<fb, 256, 0, stream>>>(b, g.present, L0.present_words, c->C, mul);
+    ARA_CUDA(cudaGetLastError());
+    g.folds.push_back({fw, mul, b});
+    fold = b;
+  }
+  FusedParams p;
+  memset(&p, 0, sizeof p);
+  p.ids = ids;
+  p.num_trials = num_trials;
+  p.num_events = num_events;
+  p.K = K;
+  p.C = c->C;
+  p.present = fold;
+  p.present_words = fw;
+  p.fold_mul = mul;
+  p.rec = g.rec;
+  p.nl = nl;
+  p.prefetch = c->prefetch != 0 ? 1u : 0u;
+  p.ylt = ylt;
+  p.ld = ld;
+  p.err = c->d_err;
+  for (int j = 0; j < kFusedMaxCols; ++j) {
+    p.r1[j] = 0.0;
+    p.l1[j] = INFINITY;
+  }
+  uint32_t col = 0;
+  for (uint32_t i = 0; i < nl; ++i) {
+    const Layer& L = c->layers[g.l0 + i];
+    p.table[i] = L.table;
+    p.jpad[i] = L.jpad;
+    p.J[i] = L.J;
+    p.col0[i] = col;
+    p.r2[i] = L.r2;
+    p.l2[i] = L.l2;
+    p.r3[i] = L.r3;
+    p.l3[i] = L.l3;
+    for (uint32_t j = 0; j < L.J; ++j) {
+      p.r1[col + j] = L.r1[j];
+      p.l1[col + j] = L.l1[j];
+      p.layer_of[col + j] = (uint8_t)i;
+    }
+    col += L.J;
+  }
+  const size_t dyn = (size_t)fw * 4 + fused_smem_extra(NW, nl);
+  st = fn_dyn_smem(c, fn, dyn);
+  if (st) return st;
+  uint64_t blocks = (uint64_t)c->sms;
+  const uint64_t need = (num_trials + NW - 1) / NW;
+  if (blocks > need) blocks = need;
+  c->last_kernel = "ara_fused_kernel<NW=16>";
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = stream;
+  ARA_CUDA(cudaLaunchKernelEx(&cfg, ara_fused_kernel<NW>, p));
+  return ARA_OK;
+}
+
 static ara_status run_layers(ara_ctx* c, const uint32_t* ids, const uint64_t* offsets, uint64_t num_trials,
                              uint64_t num_events, uint32_t K, double* ylt, double* olt, uint64_t ld, cudaStream_t s) {
+  // one pass over the YET per layer group (fixed-length trials, every layer on the sparse path)
+  bool fuse = c->fused > 0 && !olt && c->layers.size() >= 2 && num_trials > 0 &&
+              stream_eligible(c, ids, offsets, num_trials, K, 16) && c->kernel < 0 && !c->precombined &&
+              c->stream_kernel == 0;
+  for (size_t l = 0; fuse && l < c->layers.size(); ++l) fuse = !c->layers[l].xs_auto;  // not for heavily folded layers
+  if (fuse) {
+    if (!c->groups_built) {
+      ara_status st = build_groups(c, s);
+      if (st) return st;
+    }
+    for (auto& g : c->groups) {
+      ara_status st = (g.l1 - g.l0 >= 2)
+                          ? launch_fused(c, g, ids, num_trials, num_events, K, ylt + g.l0 * ld, ld, s)
+                          : launch_layer(c, c->layers[g.l0], ids, offsets, num_trials, num_events, K, ylt + g.l0 * ld,
+                                         nullptr, s);
+      if (st) return st;
+    }
+    return ARA_OK;
+  }
   for (size_t l = 0; l < c->layers.size(); ++l) {
     ara_status st = launch_layer(c, c->layers[l], ids, offsets, num_trials, num_events, K, ylt + l * ld,
                                  olt ? olt + l * ld : nullptr, s);
@@ -1090,6 +1306,10 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
       if (v < 0 || v > 1) return set_error(ARA_E_ARG, "precombined in {0, 1}");
       c->precombined = (int)v;
       return ARA_OK;
+    case ARA_OPT_FUSED:
+      if (v < 0 || v > 1) return set_error(ARA_E_ARG, "fused in {0, 1}");
+      c->fused = (int)v;
+      return ARA_OK;
     case ARA_OPT_TRIAL_ORDER:
       if (v < 0 || v > 1) return set_error(ARA_E_ARG, "trial order in {0 blocks, 1 interleaved}");
       c->interleave = (int)v;
@@ -1124,6 +1344,7 @@ ara_status ara_get_option(ara_ctx* c, ara_option opt, int64_t* v) {
     case ARA_OPT_STREAM: *v = c->stream_kernel; return ARA_OK;
     case ARA_OPT_ROUND_MIN: *v = c->round_min; return ARA_OK;
     case ARA_OPT_TRIAL_ORDER: *v = c->interleave; return ARA_OK;
+    case ARA_OPT_FUSED: *v = c->fused; return ARA_OK;
   }
   return set_error(ARA_E_ARG, "unknown option %d", (int)opt);
 }

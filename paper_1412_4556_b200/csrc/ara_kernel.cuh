@@ -171,8 +171,11 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
 __device__ __forceinline__ void cp_async8(uint32_t saddr, const void* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(saddr), "l"(g) : "memory");
 }
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(saddr), "l"(g), "l"(pol) : "memory");
+// (The L2 cache-policy operand is not used: ptxas 12.9 sometimes encodes the cache-hinted LDGSTS with an
+// odd-numbered uniform descriptor register next to a uniform shared-address offset -- an illegal
+// instruction at run time, seen on the FX and stream kernels.)
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint64_t /*pol*/) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(saddr), "l"(g) : "memory");
 }
 // Streaming 16-byte load of 4 YET ids with no L2 policy operand (L1 no-allocate).
 __device__ __forceinline__ uint4 ld_ids4_stream(const uint32_t* p) {

@@ -252,19 +252,22 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
       test_enqueue(v.w, C, fmul, bits_s, valid, q_l, tail);
     }
     // rounds: enough lanes hold a hit, or a queue could overflow in the next window (<= 4 more; a queue
-    // of 8 entries takes them while it holds <= 4)
-    const uint32_t full = __ballot_sync(FULL, tail - head >= (kLaneQ - 3u) * 128u);
-    if (full != 0u || (uint32_t)__popc(__ballot_sync(FULL, tail != head)) >= round_min) {
+    // of 8 entries takes them while it holds <= 4).  One call site, so one copy of the round's code.
+    bool go = __any_sync(FULL, tail - head >= (kLaneQ - 3u) * 128u) ||
+              (uint32_t)__popc(__ballot_sync(FULL, tail != head)) >= round_min;
+    while (go) {
       round();
-      while (__any_sync(FULL, tail - head >= (kLaneQ - 3u) * 128u)) round();
+      go = __any_sync(FULL, tail - head >= (kLaneQ - 3u) * 128u);
     }
   };
 
-  const uint32_t nfull = nwin - 1u;  // full windows per trial before the lane-masked tail window
-  const uint32_t npair = nfull >> 1;
+  // Window loop: one scan site (the window's successor is requested first -- the next window of the
+  // trial, or the first window of the warp's next trial after the lane-masked tail window -- and the
+  // buffers are rotated by moves), so the hot code stays small.
   const uint32_t* lp = p.ids + t0 * K + 4u * lane;  // this lane's slots of the trial's first window
-  uint4 A = make_uint4(0u, 0u, 0u, 0u), B = A;
-  if (nfull != 0u || lane_last) A = ld_ids4_stream(lp);
+  const uint64_t tstride = tstep * K;
+  uint4 A = make_uint4(0u, 0u, 0u, 0u);
+  if (nwin > 1u || lane_last) A = ld_ids4_stream(lp);
   for (uint32_t k = 0; k < nt; ++k) {
     // ---- trial start: trial k-2 (parity k & 1) must be complete -- no queued or in-flight hit of it
     // -- before its parity is reused; close it, then every queued hit belongs to trial k-1
@@ -274,24 +277,17 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
     }
     pb = (tail - head) >> 7;
     curpar = k & 1u;
-    if (p.prefetch && lane == 0 && k + 2u < nt) prefetch_l2_bulk(lp + 2u * tstep * K - 4u * lane, K * 4u);
-    // ---- the trial's windows (A holds the next one; pairs of full windows alternate A and B)
-    const uint32_t* wp = lp;
-    for (uint32_t i = 0; i < npair; ++i, wp += 256) {
-      B = ld_ids4_stream(wp + 128);  // window 2i+1 < nfull: full
-      scan(A, FULL);
-      if (2u * i + 2u < nfull || lane_last) A = ld_ids4_stream(wp + 256);  // full, or the tail window
-      scan(B, FULL);
+    if (p.prefetch && lane == 0 && k + 2u < nt) prefetch_l2_bulk(lp + 2u * tstride - 4u * lane, K * 4u);
+    for (uint32_t w = 0; w < nwin; ++w) {
+      const bool last = w + 1u == nwin;
+      const uint32_t* nx = last ? lp + tstride : lp + 128u * (w + 1u);
+      const bool ok = last ? (k + 1u < nt && (nwin > 1u || lane_last)) : (w + 2u < nwin || lane_last);
+      uint4 nxt = A;
+      if (ok) nxt = ld_ids4_stream(nx);
+      scan(A, last ? last_valid : FULL);
+      A = nxt;
     }
-    if (nfull & 1u) {  // one more full window (in A); the tail window follows it
-      if (lane_last) B = ld_ids4_stream(wp + 128);
-      scan(A, FULL);
-      A = B;
-    }
-    lp += tstep * K;
-    if (k + 1u < nt && (nfull != 0u || lane_last)) B = ld_ids4_stream(lp);  // next trial's first window
-    scan(A, last_valid);  // the tail window
-    A = B;
+    lp += tstride;
     if constexpr (XS) {  // the trial's last window: its exact hits before the trial boundary
       flush_pending();
       while (__any_sync(FULL, tail - head >= (kLaneQ - 3u) * 128u)) round();

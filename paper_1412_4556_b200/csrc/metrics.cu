@@ -272,6 +272,11 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
   __shared__ int s_q2slot[kMaxQ], s_nslot;
   __shared__ double wsum[kFusedBlock / 32][kMaxQ];
   __shared__ unsigned long long wcnt[kFusedBlock / 32][kMaxQ];
+  __shared__ uint32_t s_nact, s_nnext;
+  // ACTIVE key lists (cached case): after a pass only the keys that fed some slot's histogram can
+  // matter to the next passes, so each pass scans the previous pass's survivors only (indices into the
+  // cached keys; the tail still reads every key)
+  uint16_t* act[2] = {reinterpret_cast<uint16_t*>(skeys + kCacheKeys), reinterpret_cast<uint16_t*>(skeys + kCacheKeys) + kCacheKeys};
   const unsigned FULL = 0xffffffffu;
   const unsigned nb = gridDim.x;
   const uint64_t lo = n * blockIdx.x / nb, hi = n * (blockIdx.x + 1) / nb;
@@ -288,17 +293,24 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
   if (threadIdx.x == 0) {
     s_nslot = 1;
     s_slot_prefix[0] = 0;
+    s_nact = cnt;
   }
   __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
   for (int pass = 0; pass < 8; ++pass) {
     const int ns = s_nslot;
     for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) sh[i / 256][i % 256] = 0;
+    if (threadIdx.x == 0) s_nnext = 0;
     __syncthreads();
     const int shift = 56 - 8 * pass;
-    for (uint32_t base = 0; base < cnt; base += blockDim.x) {  // warp-uniform trip count
+    const uint32_t nact = cached ? s_nact : cnt;
+    const uint16_t* cur = act[pass & 1];
+    uint16_t* nxt = act[(pass + 1) & 1];
+    for (uint32_t base = 0; base < nact; base += blockDim.x) {  // warp-uniform trip count
       const uint32_t i = base + threadIdx.x;
-      const bool valid = i < cnt;
-      const uint64_t key = valid ? (cached ? skeys[i] : to_key(y[lo + i])) : 0;
+      const bool valid = i < nact;
+      const uint32_t idx = (pass == 0 || !cached) ? i : (valid ? cur[i] : 0u);
+      const uint64_t key = valid ? (cached ? skeys[idx] : to_key(y[lo + idx])) : 0;
       const unsigned digit = (unsigned)(key >> shift) & 0xffu;
       const uint64_t hik = pass == 0 ? 0 : (key >> (shift + 8));
       // the slots' prefixes are distinct, so a key feeds at most one slot's histogram
@@ -306,12 +318,20 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
       if (valid)
         for (int j = 0; j < ns; ++j)
           if (hik == s_slot_prefix[j]) sl = j;
-      if (!__any_sync(FULL, sl >= 0)) continue;
+      const unsigned keep = __ballot_sync(FULL, sl >= 0);
+      if (keep == 0u) continue;
+      if (cached) {  // survivors of this pass (order is irrelevant to the histograms)
+        uint32_t at = 0;
+        if (lane == __ffs(keep) - 1) at = atomicAdd(&s_nnext, (uint32_t)__popc(keep));
+        at = __shfl_sync(FULL, at, __ffs(keep) - 1);
+        if (sl >= 0) nxt[at + __popc(keep & lt)] = (uint16_t)idx;
+      }
       const unsigned bin = sl >= 0 ? ((unsigned)sl << 8 | digit) : 0xffffffffu;
       const unsigned peers = __match_any_sync(FULL, bin);  // warp-aggregated shared atomics
       if (sl >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&sh[sl][digit], __popc(peers));
     }
     __syncthreads();
+    if (threadIdx.x == 0) s_nact = s_nnext;
     unsigned int(*H)[256] = st->H[pass % 3];
     for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) {
       const unsigned v = sh[i / 256][i % 256];
@@ -454,7 +474,7 @@ static const FusedInfo& fused_info() {
   if (!f.ready) {
     cudaDeviceGetAttribute(&f.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&f.coop, cudaDevAttrCooperativeLaunch, dev);
-    const size_t dyn = (size_t)kCacheKeys * sizeof(uint64_t);
+    const size_t dyn = (size_t)kCacheKeys * (sizeof(uint64_t) + 2 * sizeof(uint16_t));
     cudaFuncSetAttribute((const void*)metrics_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f.occ, (const void*)metrics_fused, kFusedBlock, dyn) != cudaSuccess) {
       cudaGetLastError();
@@ -474,7 +494,7 @@ static bool metrics_fused_batch(const double* ylt, uint64_t n, int mq, const uin
   *err = cudaSuccess;
   const FusedInfo& f = fused_info();
   if (!f.coop || f.occ < 1) return false;
-  const size_t dyn = (size_t)kCacheKeys * sizeof(uint64_t);
+  const size_t dyn = (size_t)kCacheKeys * (sizeof(uint64_t) + 2 * sizeof(uint16_t));
   uint64_t grid = (uint64_t)f.sms * f.occ;
   const uint64_t need = (n + kFusedBlock - 1) / kFusedBlock;
   if (grid > need) grid = need;

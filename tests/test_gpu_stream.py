@@ -250,3 +250,81 @@ def test_exact_scan_filter_config_x_sampled(cuda_device):
     sample = np.arange(0, N, 40)
     want = oracle.ylt_for(cfg, elts, synth.make_yet_trials(cfg, sample))
     assert np.all(within_tol(got[:, sample], want))
+
+
+# ------------------------------------------------------------------ fused multi-layer pass
+def _layers_distinct(J_list, C, seed, integer=True, shared=False, n=800):
+    """Layers over distinct ELTs (config M's reading c20), or all over the same ELTs (`shared`, the tower)."""
+    rng = np.random.default_rng(seed)
+    elts, layers, e0 = [], [], 0
+    for li, J in enumerate(J_list):
+        if not shared or li == 0:
+            for j in range(J):
+                ids = rng.choice(np.arange(1, C + 1), size=n, replace=False).astype(np.uint32)
+                losses = (rng.integers(1, 1 << 20, size=n) if integer else rng.random(n) * 1e6 + 0.5).astype(np.float32)
+                r = float(rng.integers(0, 1 << 16)) + (0.0 if integer else 0.25)
+                elts.append((ids, losses, (r, INF if j % 3 == 1 else float(rng.integers(1 << 18, 1 << 21)))))
+        idx = list(range(J)) if shared else list(range(e0, e0 + J))
+        e0 += 0 if shared else J
+        layers.append((idx, (float(1000 * li), float((li + 2) << 21)), (float(5e4 * li), 4e6 + 1e6 * li)))
+    return elts, layers
+
+
+@pytest.mark.parametrize("J_list,shared", [([16] * 8, False), ([3, 16, 1, 40, 7], False), ([16] * 20, False),
+                                           ([16] * 4, True)])
+def test_fused_layers_bitwise(cuda_device, J_list, shared):
+    """One pass for several layers: integer regime bitwise vs the oracle (distinct ELTs as config M; mixed
+    widths; 20 layers = two fused groups; a tower of layers sharing ELTs, whose events hold > 4 entries and
+    take the full-row path), and bitwise equal to layer-outer runs of the single-layer lane kernel in the
+    real regime (the same per-layer summation order)."""
+    C, K, N = 20_000, 1000, 1200
+    elts, layers = _layers_distinct(J_list, C, seed=len(J_list) + 7 * shared)
+    rng = np.random.default_rng(5)
+    yet = rng.integers(1, C + 1, size=N * K).astype(np.uint32)
+    want = oracle.ylt(C, yet, None, N, K, elts, layers)
+    ctx = _ctx(C, elts, layers)
+    select(ctx, ara.KERNEL_AUTO)
+    ctx.ara_set_option(ara.ARA_OPT_FUSED, 1)
+    got = gpu_ylt(None, ctx, yet, K=K, num_trials=N, num_layers=len(layers))
+    assert ctx.ara_kernel_name().startswith("ara_fused_kernel"), ctx.ara_kernel_name()
+    assert np.array_equal(got, want)
+    ctx.ara_set_option(ara.ARA_OPT_FUSED, 0)
+    assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N, num_layers=len(layers)), want)
+    ctx.close()
+    # real regime: fused == layer-outer lane kernel, bit for bit
+    elts, layers = _layers_distinct(J_list, C, seed=3, integer=False, shared=shared)
+    ctx = _ctx(C, elts, layers)
+    select(ctx, ara.KERNEL_AUTO)
+    ctx.ara_set_option(ara.ARA_OPT_FUSED, 1)
+    fused = gpu_ylt(None, ctx, yet, K=K, num_trials=N, num_layers=len(layers))
+    assert ctx.ara_kernel_name().startswith("ara_fused_kernel")
+    select(ctx, KERNEL_STREAM, 0)
+    outer = gpu_ylt(None, ctx, yet, K=K, num_trials=N, num_layers=len(layers))
+    assert ctx.ara_kernel_name().startswith("ara_lane_kernel")
+    assert np.array_equal(fused, outer)
+    assert np.all(within_tol(fused, oracle.ylt(C, yet, None, N, K, elts, layers)))
+
+
+def test_fused_config_m_sampled(cuda_device):
+    """Config M (8 layers x 16 distinct ELTs, real regime) on 30,000 device-generated trials: the fused
+    pass within tolerance of the oracle on sampled trials and within 1e-12 relative of the layer-outer
+    presence kernel everywhere."""
+    cfg = synth.Config.load("M")
+    elts = synth.make_elts(cfg)
+    N, K, L = 30_000, cfg.kmin, len(cfg.layers)
+    ids = torch.empty(N * K, dtype=torch.int32, device=cuda_device)
+    synth.yet_ids_device(ids.data_ptr(), cfg.seed, cfg.catalog_size, 0, N * K, torch.cuda.current_stream().cuda_stream)
+    ctx = ara.context_for_config(cfg, elts)
+    ctx.ara_set_option(ara.ARA_OPT_FUSED, 1)
+    y = torch.zeros((L, N), dtype=torch.float64, device=cuda_device)
+    ctx.ara_run(ids, y, events_per_trial=K, num_trials=N)
+    ctx.ara_check()
+    assert ctx.ara_kernel_name().startswith("ara_fused_kernel")
+    fused = y.cpu().numpy()
+    ctx.ara_set_option(ara.ARA_OPT_FUSED, 0)
+    ctx.ara_run(ids, y, events_per_trial=K, num_trials=N)
+    ctx.ara_check()
+    assert np.all(within_tol(fused, y.cpu().numpy(), rel=1e-12, abs_floor=1e-6))
+    sample = np.arange(0, N, 60)
+    want = oracle.ylt_for(cfg, elts, synth.make_yet_trials(cfg, sample))
+    assert np.all(within_tol(fused[:, sample], want))
