@@ -340,6 +340,8 @@ def main():
         if m and (world == 1 or rank == 0):
             for l in range(L):
                 ara.ara_pml_tvar_device(full[l], rps, pml_dev[l], tvar_dev[l], stream=stream)
+        if evs is not None:
+            evs[2].record(stream)
         if m and (world == 1 or rank == 0):
             met[:, 0].copy_(pml_dev, non_blocking=True)
             met[:, 1].copy_(tvar_dev, non_blocking=True)
@@ -397,7 +399,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region (warm: the table stays L2-resident; the 4 GB YET streams from HBM)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk.mark_start()
     start.record(stream)
@@ -411,11 +413,13 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     total_ms = start.elapsed_time(end)
-    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
-    t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b, _ in kev]))
+    post_ms = float(np.mean([b.elapsed_time(c) for _, b, c in kev]))  # gather + PML/TVaR
+    step_ms_list = [kev[i][0].elapsed_time(kev[i + 1][0]) for i in range(len(kev) - 1)]
+    t = torch.tensor([total_ms, kern_ms, post_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, kern_ms = float(t[0]), float(t[1])
+    total_ms, kern_ms, post_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = total_ms / args.steps
     ctx.ara_check(stream)
 
@@ -649,7 +653,10 @@ def main():
                    "kernel": kernel_full, "storage": "fp32 ELT losses, fp64 terms/sums/YLT"},
         "trials_per_s": N / (ms_per_step * 1e-3),
         "elt_lookups_per_s": lookups_exact / (ms_per_step * 1e-3),
-        "kernel_ms_per_step": kern_ms, "create_ms": create_ms, "cold_l2_ms_per_step": cold_ms,
+        "kernel_ms_per_step": kern_ms, "gather_metrics_ms_per_step": post_ms,
+        "step_ms_min_median_max": [round(float(np.min(step_ms_list)), 4), round(float(np.median(step_ms_list)), 4),
+                                   round(float(np.max(step_ms_list)), 4)] if step_ms_list else None,
+        "create_ms": create_ms, "cold_l2_ms_per_step": cold_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": kernel_name,
                      "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": launch_ms,
@@ -684,7 +691,8 @@ def study(ctx, cfg, ids, offsets_d, offsets_h, K, n_local, L, ylt_local, stream,
     from paper_1412_4556_b200 import ara
     J = sum(len(l.elts) for l in cfg.layers) / L
     for layout, name in ((ara.STUDY_INTERLEAVED, "interleaved"), (ara.STUDY_INDEPENDENT, "independent"),
-                         (ara.STUDY_SORTED, "sorted+binary-search")):
+                         (ara.STUDY_SORTED, "sorted+binary-search"), (ara.STUDY_HASH, "hash"),
+                         (ara.STUDY_INDEX, "event->compact-row index")):
         n = n_local if layout != ara.STUDY_SORTED else max(1, n_local // 16)
         if offsets_d is None:
             sub_ids, sub_off = ids[: n * K], None

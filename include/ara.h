@@ -174,10 +174,19 @@ ARA_API ara_status ara_tvar(const double* ylt, uint64_t n, const double* rps, ui
  *   0 ARA_STUDY_INTERLEAVED  the combined event-major table (one row per event)
  *   1 ARA_STUDY_INDEPENDENT  one direct-access array per ELT (the paper's GPU choice)
  *   2 ARA_STUDY_SORTED       per-ELT arrays sorted by event id, binary search
- * The extra structures are built on first use (layout 2 copies the table to the host once).  Same
+ *   3 ARA_STUDY_HASH         per-ELT open-addressing hash tables, load factor <= 1/2 (PAPER.md:211,
+ *                            "constant-time hash search")
+ *   4 ARA_STUDY_INDEX        an event -> compact-row index plus the rows holding a loss
+ * The extra structures are built on first use (layouts 2-4 copy the table to the host once).  Same
  * YET / YLT conventions as ara_run; asynchronous except for that first build.  Invalid ids read as
  * absent and are not reported. */
-typedef enum { ARA_STUDY_INTERLEAVED = 0, ARA_STUDY_INDEPENDENT = 1, ARA_STUDY_SORTED = 2 } ara_study_layout;
+typedef enum {
+  ARA_STUDY_INTERLEAVED = 0,
+  ARA_STUDY_INDEPENDENT = 1,
+  ARA_STUDY_SORTED = 2,
+  ARA_STUDY_HASH = 3,
+  ARA_STUDY_INDEX = 4
+} ara_study_layout;
 ARA_API ara_status ara_run_study(ara_ctx* ctx, int layout, const ara_yet* yet, double* ylt, void* stream);
 
 /* Average annual loss of a DEVICE YLT of n values: the mean, reduced in a fixed order (bitwise

@@ -30,7 +30,7 @@ ARA_OPT_ROUND_MIN = 10
 ARA_OPT_TRIAL_ORDER = 11
 ARA_OPT_FUSED = 12
 KERNEL_AUTO, KERNEL_PRESENCE, KERNEL_DENSE = -1, 0, 1
-STUDY_INTERLEAVED, STUDY_INDEPENDENT, STUDY_SORTED = 0, 1, 2
+STUDY_INTERLEAVED, STUDY_INDEPENDENT, STUDY_SORTED, STUDY_HASH, STUDY_INDEX = 0, 1, 2, 3, 4
 ARA_MAX_ELTS_PER_LAYER = 128
 
 #: every symbol include/ara.h declares (checked by tests/test_abi.py against the header and the .so)

@@ -83,6 +83,11 @@ struct Layer {
   uint32_t* sorted_ids = nullptr; // per-ELT (event, loss) pairs sorted by event
   float* sorted_loss = nullptr;
   uint32_t* sorted_off = nullptr; // J + 1
+  uint2* hash = nullptr;           // STUDY_HASH tables, offsets and log2 capacities
+  uint32_t* hash_off = nullptr;
+  uint32_t* hash_bits = nullptr;
+  uint32_t* row_index = nullptr;   // STUDY_INDEX: event -> compact row, and the compact rows
+  float* compact = nullptr;
   uint32_t present_words = 0;
   std::vector<const Variant*> variants[2];  // by KernelKind
   uint64_t present_rows = 0;                // rows holding at least one loss
@@ -323,6 +328,11 @@ static void destroy_ctx(ara_ctx* c) {
     cudaFree(L.sorted_ids);
     cudaFree(L.sorted_loss);
     cudaFree(L.sorted_off);
+    cudaFree(L.hash);
+    cudaFree(L.hash_off);
+    cudaFree(L.hash_bits);
+    cudaFree(L.row_index);
+    cudaFree(L.compact);
   }
   for (auto& g : c->groups) {
     cudaFree(g.rec);
@@ -1168,7 +1178,7 @@ ara_status ara_run_host(ara_ctx* c, const ara_yet* yet, double* ylt_host, void* 
 
 ara_status ara_run_study(ara_ctx* c, int layout, const ara_yet* yet, double* ylt, void* stream) {
   if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
-  if (layout < STUDY_INTERLEAVED || layout > STUDY_SORTED) return set_error(ARA_E_ARG, "unknown layout %d", layout);
+  if (layout < STUDY_INTERLEAVED || layout > STUDY_INDEX) return set_error(ARA_E_ARG, "unknown layout %d", layout);
   ara_status st = check_yet(yet);
   if (st) return st;
   if (yet->num_trials == 0) return ARA_OK;
@@ -1210,9 +1220,66 @@ ara_status ara_run_study(ara_ctx* c, int layout, const ara_yet* yet, double* ylt
       ARA_CUDA(cudaMemcpy(L.sorted_loss, loss.data(), loss.size() * 4, cudaMemcpyHostToDevice));
       ARA_CUDA(cudaMemcpy(L.sorted_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
     }
+    if ((layout == STUDY_HASH && !L.hash) || (layout == STUDY_INDEX && !L.row_index)) {
+      std::vector<float> h(rows * L.jpad);
+      ARA_CUDA(cudaStreamSynchronize(s));
+      ARA_CUDA(cudaMemcpy(h.data(), L.table, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+      if (layout == STUDY_HASH) {  // per ELT: capacity = smallest power of two >= 2 n (load factor <= 1/2)
+        std::vector<uint32_t> off(L.J + 1, 0), bits(L.J, 1);
+        std::vector<uint2> tab;
+        for (uint32_t j = 0; j < L.J; ++j) {
+          uint64_t n = 0;
+          for (uint64_t e = 1; e < rows; ++e) n += h[e * L.jpad + j] != 0.0f;
+          uint32_t b = 1;
+          while ((1ull << b) < 2 * n + 2) ++b;
+          bits[j] = b;
+          const size_t base = tab.size();
+          tab.resize(base + (1ull << b), make_uint2(0u, 0u));
+          for (uint64_t e = 1; e < rows; ++e) {
+            const float x = h[e * L.jpad + j];
+            if (x == 0.0f) continue;
+            uint32_t k = ((uint32_t)e * 0x9E3779B1u) >> (32u - b);
+            while (tab[base + k].x != 0u) k = (k + 1u) & ((1u << b) - 1u);
+            uint32_t bitsx;
+            memcpy(&bitsx, &x, 4);
+            tab[base + k] = make_uint2((uint32_t)e, bitsx);
+          }
+          off[j + 1] = (uint32_t)tab.size();
+        }
+        if (cudaMalloc(&L.hash, tab.size() * sizeof(uint2)) != cudaSuccess ||
+            cudaMalloc(&L.hash_off, off.size() * 4) != cudaSuccess || cudaMalloc(&L.hash_bits, bits.size() * 4) != cudaSuccess) {
+          cudaGetLastError();
+          return set_error(ARA_E_NOMEM, "hash tables");
+        }
+        ARA_CUDA(cudaMemcpy(L.hash, tab.data(), tab.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+        ARA_CUDA(cudaMemcpy(L.hash_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+        ARA_CUDA(cudaMemcpy(L.hash_bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
+      } else {  // event -> compact row; compact row 0 is the zero row
+        std::vector<uint32_t> idx(rows, 0u);
+        std::vector<float> comp(L.jpad, 0.0f);
+        for (uint64_t e = 1; e < rows; ++e) {
+          bool any = false;
+          for (uint32_t j = 0; j < L.jpad; ++j) any |= h[e * L.jpad + j] != 0.0f;
+          if (!any) continue;
+          idx[e] = (uint32_t)(comp.size() / L.jpad);
+          comp.insert(comp.end(), h.begin() + e * L.jpad, h.begin() + (e + 1) * L.jpad);
+        }
+        if (cudaMalloc(&L.row_index, rows * 4) != cudaSuccess || cudaMalloc(&L.compact, comp.size() * 4) != cudaSuccess) {
+          cudaGetLastError();
+          return set_error(ARA_E_NOMEM, "compact rows");
+        }
+        ARA_CUDA(cudaMemcpy(L.row_index, idx.data(), rows * 4, cudaMemcpyHostToDevice));
+        ARA_CUDA(cudaMemcpy(L.compact, comp.data(), comp.size() * 4, cudaMemcpyHostToDevice));
+      }
+    }
     StudyParams p;
     memset(&p, 0, sizeof p);
     p.table = L.table;
+    p.hash = L.hash;
+    p.hash_off = L.hash_off;
+    p.hash_bits = L.hash_bits;
+    p.row_index = L.row_index;
+    p.compact = L.compact;
     p.indep = L.indep;
     p.sorted_ids = L.sorted_ids;
     p.sorted_loss = L.sorted_loss;

@@ -8,6 +8,10 @@
 //                      table"; the paper's faster layout on its M2050)
 //   STUDY_SORTED       per ELT the (event, loss) pairs sorted by event id, found by binary search
 //                      ("binary search require O(log(n)) memory accesses")
+//   STUDY_HASH         per ELT an open-addressing hash table of (event, loss) pairs, load factor <= 1/2,
+//                      multiplicative hash, linear probing ("constant-time hash search")
+//   STUDY_INDEX        an event -> compact-row index over the layer (one u32 per event) and a table of the
+//                      rows that hold a loss (~154k rows for P instead of 2M)
 // The loops are deliberately plain: the point is the memory behaviour of each representation
 // (sectors per lookup, DRAM traffic), measured by bench.py --study and ncu.
 #include <cuda_runtime.h>
@@ -24,6 +28,19 @@ __device__ __forceinline__ float study_lookup(const StudyParams& p, uint32_t e, 
     return __ldg(p.table + (uint64_t)e * p.jpad + j);
   } else if constexpr (LAYOUT == STUDY_INDEPENDENT) {
     return __ldg(p.indep + (uint64_t)j * p.rows + e);
+  } else if constexpr (LAYOUT == STUDY_HASH) {
+    const uint2* t = p.hash + p.hash_off[j];
+    const uint32_t bits = p.hash_bits[j], mask = (1u << bits) - 1u;
+    uint32_t h = (e * 0x9E3779B1u) >> (32u - bits);
+    while (true) {  // an empty slot (id 0) ends the probe: the event is absent from this ELT
+      const uint2 v = __ldg(t + h);
+      if (v.x == e) return __uint_as_float(v.y);
+      if (v.x == 0u) return 0.0f;
+      h = (h + 1u) & mask;
+    }
+  } else if constexpr (LAYOUT == STUDY_INDEX) {
+    const uint32_t r = __ldg(p.row_index + e);  // 0: the event holds no loss (row 0 is all zero)
+    return __ldg(p.compact + (uint64_t)r * p.jpad + j);
   } else {
     const uint32_t* ids = p.sorted_ids + p.sorted_off[j];
     const float* losses = p.sorted_loss + p.sorted_off[j];
@@ -73,6 +90,8 @@ void* study_kernel_fn(int layout) {
     case STUDY_INTERLEAVED: return (void*)study_kernel<STUDY_INTERLEAVED>;
     case STUDY_INDEPENDENT: return (void*)study_kernel<STUDY_INDEPENDENT>;
     case STUDY_SORTED: return (void*)study_kernel<STUDY_SORTED>;
+    case STUDY_HASH: return (void*)study_kernel<STUDY_HASH>;
+    case STUDY_INDEX: return (void*)study_kernel<STUDY_INDEX>;
   }
   return nullptr;
 }

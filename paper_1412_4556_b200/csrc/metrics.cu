@@ -472,6 +472,14 @@ static const FusedInfo& fused_info() {
   cudaGetDevice(&dev);
   FusedInfo& f = g_fused[dev & 63];
   if (!f.ready) {
+    // the per-call metric scratch comes from the device's stream-ordered pool: keep freed blocks in the
+    // pool (no trimming at synchronisation points), so a call never goes back to the driver for memory
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
     cudaDeviceGetAttribute(&f.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&f.coop, cudaDevAttrCooperativeLaunch, dev);
     const size_t dyn = (size_t)kCacheKeys * (sizeof(uint64_t) + 2 * sizeof(uint16_t));

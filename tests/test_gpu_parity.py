@@ -505,7 +505,8 @@ def test_metrics_device_outputs_async(cuda_device):
         ara.ara_pml_tvar_device(ds[0], [n * 2.0], outs[0][0], None)
 
 
-@pytest.mark.parametrize("layout", [ara.STUDY_INTERLEAVED, ara.STUDY_INDEPENDENT, ara.STUDY_SORTED])
+@pytest.mark.parametrize("layout", [ara.STUDY_INTERLEAVED, ara.STUDY_INDEPENDENT, ara.STUDY_SORTED, ara.STUDY_HASH,
+                                    ara.STUDY_INDEX])
 def test_section_4b_study_layouts(cuda_device, layout):
     """The Section IV.B data-structure study kernels compute the same YLT."""
     for J, kw in ((16, {}), (3, {}), (24, dict(seed=5))):
