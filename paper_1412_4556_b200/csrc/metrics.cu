@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
   // ACTIVE key lists (cached case): after a pass only the keys that fed some slot's histogram can
   // matter to the next passes, so each pass scans the previous pass's survivors only (indices into the
   // cached keys; the tail still reads every key)
-  uint16_t* act[2] = {reinterpret_cast<uint16_t*>(skeys + kCacheKeys), reinterpret_cast<uint16_t*>(skeys + kCacheKeys) + kCacheKeys};
+  const uint32_t act_s = (uint32_t)__cvta_generic_to_shared(skeys + kCacheKeys);  // two u16 lists of kCacheKeys
   const unsigned FULL = 0xffffffffu;
   const unsigned nb = gridDim.x;
   const uint64_t lo = n * blockIdx.x / nb, hi = n * (blockIdx.x + 1) / nb;
@@ -304,12 +304,17 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
     __syncthreads();
     const int shift = 56 - 8 * pass;
     const uint32_t nact = cached ? s_nact : cnt;
-    const uint16_t* cur = act[pass & 1];
-    uint16_t* nxt = act[(pass + 1) & 1];
+    const uint32_t cur_s = act_s + (uint32_t)(pass & 1) * (kCacheKeys * 2u);
+    const uint32_t nxt_s = act_s + (uint32_t)((pass + 1) & 1) * (kCacheKeys * 2u);
     for (uint32_t base = 0; base < nact; base += blockDim.x) {  // warp-uniform trip count
       const uint32_t i = base + threadIdx.x;
       const bool valid = i < nact;
-      const uint32_t idx = (pass == 0 || !cached) ? i : (valid ? cur[i] : 0u);
+      uint32_t idx = i;
+      if (pass != 0 && cached && valid) {
+        unsigned short v16;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v16) : "r"(cur_s + 2u * i) : "memory");
+        idx = v16;
+      }
       const uint64_t key = valid ? (cached ? skeys[idx] : to_key(y[lo + idx])) : 0;
       const unsigned digit = (unsigned)(key >> shift) & 0xffu;
       const uint64_t hik = pass == 0 ? 0 : (key >> (shift + 8));
@@ -324,7 +329,9 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
         uint32_t at = 0;
         if (lane == __ffs(keep) - 1) at = atomicAdd(&s_nnext, (uint32_t)__popc(keep));
         at = __shfl_sync(FULL, at, __ffs(keep) - 1);
-        if (sl >= 0) nxt[at + __popc(keep & lt)] = (uint16_t)idx;
+        if (sl >= 0)
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(nxt_s + 2u * (at + __popc(keep & lt))), "h"((unsigned short)idx)
+                       : "memory");
       }
       const unsigned bin = sl >= 0 ? ((unsigned)sl << 8 | digit) : 0xffffffffu;
       const unsigned peers = __match_any_sync(FULL, bin);  // warp-aggregated shared atomics
@@ -405,26 +412,37 @@ __global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __res
     }
     __syncthreads();
   }
-  // tail: count and fp64-sum the values above each query's threshold T (fixed reduction order), one
-  // query at a time so each thread holds a single accumulator pair
-  for (int q = 0; q < m; ++q) {
-    const uint64_t pq = s_prefix[q];
-    double a = 0.0;
-    unsigned long long b = 0;
+  // tail: count and fp64-sum the values above each query's threshold T (fixed reduction order), four
+  // queries per sweep over the keys (each key decoded once per sweep; every query still adds its keys
+  // in the same thread order as a query-at-a-time loop)
+  for (int q0 = 0; q0 < m; q0 += 4) {
+    uint64_t pq[4];
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    uint32_t b[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pq[j] = q0 + j < m ? s_prefix[q0 + j] : ~0ull;  // no key exceeds ~0
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
       const uint64_t key = cached ? skeys[i] : to_key(y[lo + i]);
-      if (key > pq) {
-        a += from_key(key);
-        b += 1;
+      const double v = from_key(key);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (key > pq[j]) {
+          a[j] += v;
+          b[j] += 1u;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double aj = a[j];
+      unsigned long long bj = b[j];
+      for (int off = 16; off > 0; off >>= 1) {
+        aj += __shfl_xor_sync(FULL, aj, off);
+        bj += __shfl_xor_sync(FULL, bj, off);
       }
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-      a += __shfl_xor_sync(FULL, a, off);
-      b += __shfl_xor_sync(FULL, b, off);
-    }
-    if (lane == 0) {
-      wsum[w][q] = a;
-      wcnt[w][q] = b;
+      if (lane == 0 && q0 + j < m) {
+        wsum[w][q0 + j] = aj;
+        wcnt[w][q0 + j] = bj;
+      }
     }
   }
   __syncthreads();
