@@ -217,8 +217,8 @@ __device__ __forceinline__ void pair_insert(uint32_t wa, uint32_t xa, uint32_t i
       "{\n"
       " .reg .pred pa, pb, pany, pboth, pq;\n"
       " .reg .b32 sa, sb, ma, mb, f, m, t, a, c;\n"
-      " and.b32 sa, %2, 31;\n shl.b32 ma, 1, sa;\n and.b32 ma, ma, %1;\n and.b32 ma, ma, %8;\n setp.ne.b32 pa, ma, 0;\n"
-      " and.b32 sb, %5, 31;\n shl.b32 mb, 1, sb;\n and.b32 mb, mb, %4;\n and.b32 mb, mb, %8;\n setp.ne.b32 pb, mb, 0;\n"
+      " and.b32 sa, %2, 31;\n shr.b32 ma, %1, sa;\n and.b32 ma, ma, %8;\n and.b32 ma, ma, 1;\n setp.ne.b32 pa, ma, 0;\n"
+      " and.b32 sb, %5, 31;\n shr.b32 mb, %4, sb;\n and.b32 mb, mb, %8;\n and.b32 mb, mb, 1;\n setp.ne.b32 pb, mb, 0;\n"
       " or.pred pany, pa, pb;\n and.pred pboth, pa, pb;\n"
       " selp.b32 f, %3, %6, pa;\n"
       " vote.sync.ballot.b32 m, pany, 0xffffffff;\n"

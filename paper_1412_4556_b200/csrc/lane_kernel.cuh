@@ -96,7 +96,8 @@ __device__ __forceinline__ void exact_enqueue(uint32_t ew, uint32_t x, uint32_t 
 
 // NW: warps per block (one block per SM).  OLT: also the largest occurrence-net loss per trial.
 // XS: exact scan filter (see exact_enqueue).
-template <int NW, bool OLT, bool XS = false>
+// XD: windows between an exact word's load and its test (1 or 2; 2 hides more L2 latency, 8 more registers).
+template <int NW, bool OLT, bool XS = false, int XD = 1>
 __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_constant__ LayerParams p) {
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) uint32_t smem[];
@@ -219,23 +220,38 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
     if (par) S1 = 0.0; else S0 = 0.0;
   };
   // Scan one window: presence test per id, hits appended to the lane's own queue.
-  // XS: the previous window's candidates (x, exact word; a non-candidate holds word 0)
+  // XS: the previous window's candidates (x, exact word; a non-candidate holds word 0); with XD == 2 also
+  // the window before it (qx*, qw*), tested first
   uint32_t px0 = 0, px1 = 0, px2 = 0, px3 = 0, pw0 = 0, pw1 = 0, pw2 = 0, pw3 = 0;
+  uint32_t qx0 = 0, qx1 = 0, qx2 = 0, qx3 = 0, qw0 = 0, qw1 = 0, qw2 = 0, qw3 = 0;
   auto exact_load = [&](uint32_t cand, uint32_t x) -> uint32_t {
     uint32_t w = 0u;
     if (cand) w = x < C ? ld_id(p.exact + ((x + 1u) >> 5), pol_exact) : 0xffffffffu;  // invalid: forced hit
     return w;
   };
-  auto flush_pending = [&]() {  // XS: the previous window's exact hits enter the queue (in slot order)
-    exact_enqueue(pw0, px0, q_l, tail);
-    exact_enqueue(pw1, px1, q_l, tail);
-    exact_enqueue(pw2, px2, q_l, tail);
-    exact_enqueue(pw3, px3, q_l, tail);
+  auto flush_oldest = [&]() {  // XS: the oldest pending window's exact hits enter the queue (slot order)
+    if constexpr (XD == 2) {
+      exact_enqueue(qw0, qx0, q_l, tail);
+      exact_enqueue(qw1, qx1, q_l, tail);
+      exact_enqueue(qw2, qx2, q_l, tail);
+      exact_enqueue(qw3, qx3, q_l, tail);
+      qx0 = px0; qx1 = px1; qx2 = px2; qx3 = px3;
+      qw0 = pw0; qw1 = pw1; qw2 = pw2; qw3 = pw3;
+    } else {
+      exact_enqueue(pw0, px0, q_l, tail);
+      exact_enqueue(pw1, px1, q_l, tail);
+      exact_enqueue(pw2, px2, q_l, tail);
+      exact_enqueue(pw3, px3, q_l, tail);
+    }
     pw0 = pw1 = pw2 = pw3 = 0u;
+  };
+  auto flush_pending = [&]() {  // XS: every pending window, oldest first
+    flush_oldest();
+    if constexpr (XD == 2) flush_oldest();
   };
   auto scan = [&](const uint4 v, uint32_t valid) {
     if constexpr (XS) {
-      flush_pending();
+      flush_oldest();
       uint32_t c;
       c = fold_candidate(v.x, C, fmul, bits_s, valid, px0);
       pw0 = exact_load(c, px0);

@@ -586,6 +586,7 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
   char* scratch = nullptr;
   ARA_CUDA(cudaMallocAsync((void**)&scratch, bytes, s));
   double* d_out = (double*)scratch;
+  ARA_CUDA(cudaMemsetAsync(d_out, 0, 2 * kMaxQ * sizeof(double), s));  // every copied-back slot defined
   char* rest = scratch + 2 * kMaxQ * sizeof(double);
   const size_t rest_bytes = bytes - 2 * kMaxQ * sizeof(double);
   SelState* st = (SelState*)rest;

@@ -273,6 +273,8 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   __shared__ double2 s_t1[kCarry ? JPS : 1];  // record batches: FT1 as (R, L) pairs, one 16-B load per column
   __shared__ WarpTrials s_wt[NW];
   uint32_t* bits = smem;  // [present_words], already folded by the host (fold_mul)
+  uint32_t bits_s;        // its shared address, kept in a register (not rebuilt from the CTA id per window)
+  asm volatile("mov.u32 %0, %1;" : "=r"(bits_s) : "r"((uint32_t)__cvta_generic_to_shared(smem)));
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // provably warp-uniform for ptxas
   const int lane = threadIdx.x & 31;
   uint32_t* q = smem + p.present_words + warp * kQueue;
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       x[u] = min(id[u] - 1u, C);          // invalid ids -> the sentinel bit C
-      wd[u] = bits[__umulhi(x[u], fmul)];  // the folded bitmap word holding bit x & 31
+      wd[u] = lds_ro_u32(bits_s + 4u * __umulhi(x[u], fmul));  // the folded bitmap word holding bit x & 31
       if constexpr (decltype(checked)::value) wd[u] = (r + (uint32_t)u < len) ? wd[u] : 0u;  // outside the trial
     }
     // Append the hits in a fixed order that depends only on the window: per pair of slots, first the
