@@ -238,8 +238,9 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           staged in shared memory, so only rows that hold a loss are gathered;
  *                           1 dense: every occurrence gathers its full row.  The same YLT up to
  *                           the fp64 summation order (an all-zero row contributes exactly 0, PAPER.md:209,
- *                           reading c9): bitwise identical in the integer regime, within ~1e-12
- *                           relative otherwise (each kernel's order is fixed, so each is reproducible).
+ *                           reading c9): bitwise identical in the integer regime, equal to the rounding
+ *                           of the summation order otherwise (each kernel's order is fixed, so each is
+ *                           reproducible).
  *                           Selecting a kernel resets ARA_OPT_VARIANT to 0.
  *   ARA_OPT_FILTER          presence kernel, one lane per row: -1 auto (default; = off), 0 off, 1 on.
  *                           The exact filter stage checks every candidate of the folded shared-memory
@@ -260,7 +261,8 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           kernel (stream_kernel.cuh: the presence kernel's summation order); 0 =
  *                           always the presence kernel.  Every kernel's order is fixed: the YLT is
  *                           reproducible bit for bit and independent of the sharding; across kernels it
- *                           agrees bitwise in the integer regime and within ~1e-12 relative otherwise.
+ *                           agrees bitwise in the integer regime and to the rounding of the summation
+ *                           order otherwise (amplified by FT3 when S_n is close to its retention).
  *   ARA_OPT_ROUND_MIN       per-lane-queue kernel: a gather round starts when at least this many lanes
  *                           hold a queued hit (1..32, 0 = default 24), or when a queue nearly fills.
  *   ARA_OPT_TRIAL_ORDER     fixed-length-trial kernels: 1 (default) trials interleaved over the grid's

@@ -17,8 +17,8 @@ namespace ara {
 
 // ARA_OPT_STREAM = index + 1; the first XS entry is the automatic choice for layers whose folded bitmap
 // nominates far more candidates than it holds rows (ARA_OPT_FILTER auto)
-static const StreamVariant kStream[] = {ARA_LANE(32),     ARA_LANE(24),    ARA_LANE(16),    ARA_RING(32),
-                                        ARA_LANE_XS2(24), ARA_LANE_XS(24), ARA_LANE_XS(32), ARA_LANE_XS(16)};
+static const StreamVariant kStream[] = {ARA_LANE(32),    ARA_LANE(24),    ARA_LANE(16),    ARA_RING(32),
+                                        ARA_LANE_XS(24), ARA_LANE_XS2(24), ARA_LANE_XS(32), ARA_LANE_XS(16)};
 
 const StreamVariant* stream_variants(int* n) {
   *n = (int)(sizeof(kStream) / sizeof(kStream[0]));
