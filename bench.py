@@ -495,7 +495,7 @@ def main():
     peak, peak_src = peaks()
     kernel_full = ctx.ara_kernel_name()  # the kernel the timed runs launched
     kernel_name = kernel_full.split("<")[0]
-    sparse_path = kernel_name in ("ara_presence_kernel", "ara_stream_kernel", "ara_lane_kernel")
+    sparse_path = kernel_name in ("ara_presence_kernel", "ara_stream_kernel", "ara_lane_kernel", "ara_mask_kernel")
     # compulsory HBM bytes of one presence-kernel launch: the YET ids (4 B per occurrence), the YLT
     # row (8 B per trial), and one read of every table row that holds a loss plus the bitmap
     present_rows = [ctx.ara_layer_stats(l)["present_rows"] for l in range(L)]
@@ -602,7 +602,7 @@ def main():
         ctx.ara_run(ids, ylt_local, offsets=offsets_d, events_per_trial=K, num_trials=n_local, stream=stream)
         ref_ylt = ylt_local.clone()  # the product path's YLT
         # the round-1 presence kernel (stream kernel off), timed beside: its YLT must equal bit for bit
-        if kernel_name in ("ara_stream_kernel", "ara_lane_kernel"):
+        if kernel_name in ("ara_stream_kernel", "ara_lane_kernel", "ara_mask_kernel"):
             ctx.ara_set_option(ara.ARA_OPT_STREAM, 0)
             ctx.ara_set_option(ara.ARA_OPT_FILTER, 0)  # the presence kernel itself (no exact scan filter)
             for _ in range(2):
@@ -729,7 +729,7 @@ def sweep(ctx, ids, offsets_d, K, n_local, L, ylt_local, stream, info, occ):
 
     from paper_1412_4556_b200 import ara
     rb = max(32, info[0]["row_stride"])
-    if info[0].get("product_kernel", "").startswith(("ara_stream", "ara_lane")):  # fixed-length-trial kernels
+    if info[0].get("product_kernel", "").startswith(("ara_stream", "ara_lane", "ara_mask")):  # fixed-length-trial kernels
         for sv in (1, 4):
             for pf in (0, 1):
                 for pol in (0, 1):  # here: the trial order (0 blocks, 1 interleaved)

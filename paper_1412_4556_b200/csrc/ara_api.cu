@@ -17,6 +17,7 @@
 #include "presence_kernel.cuh"
 #include "stream_kernel.cuh"
 #include "lane_kernel.cuh"
+#include "mask_kernel.cuh"
 #include "fused_kernel.cuh"
 #include "variants.cuh"
 #include "study.cuh"
@@ -478,7 +479,8 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   if (!svar && (c->filter == 1 || (c->filter < 0 && L.xs_auto)))  // exact scan filter for fixed-length trials
     for (int v = 0; v < nsv && !svar; ++v)
       if (sv[v].xs) svar = &sv[v];
-  if (var->kind == KIND_PRESENCE && svar && stream_eligible(c, ids, offsets, num_trials, K, svar->NW)) {
+  if (var->kind == KIND_PRESENCE && svar && stream_eligible(c, ids, offsets, num_trials, K, svar->NW) &&
+      (svar->ring != 2 || (K + 127u) / 128u == 8u)) {  // the mask kernel is built for 8 windows per trial
     // fixed-length trials: the stream kernel (stream_kernel.cuh), one block of NW warps per SM
     fn = olt ? svar->fn_olt : svar->fn;
     name = svar->name;
@@ -487,7 +489,9 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
     int st_smem = 0;
     ara_status st = fn_static_smem(c, (const void*)fn, &st_smem);
     if (st) return st;
-    const uint32_t extra = svar->ring ? stream_smem_extra(L.jpad, svar->NW) : lane_smem_extra(L.jpad, svar->NW);
+    const uint32_t extra = svar->ring == 1 ? stream_smem_extra(L.jpad, svar->NW)
+                           : svar->ring == 2 ? mask_smem_extra(L.jpad, svar->NW)
+                                             : lane_smem_extra(L.jpad, svar->NW);
     const int64_t budget = (int64_t)c->smem_optin - st_smem - (int64_t)extra;
     if (budget < 4096) return set_error(ARA_E_UNSUPPORTED, "no shared memory left for the presence bitmap");
     const uint32_t* fold = nullptr;
@@ -894,8 +898,11 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
         const StreamVariant* sv = stream_variants(&nsv);
         int64_t b = budget;
         for (int v = 0; v < nsv; ++v)
-          b = std::min<int64_t>(b, (int64_t)c->smem_optin - (int64_t)(sv[v].ring ? stream_smem_extra(L.jpad, sv[v].NW)
-                                                                                  : lane_smem_extra(L.jpad, sv[v].NW)));
+          if (sv[v].ring != 2)  // the mask kernel folds with its own (smaller) budget
+          b = std::min<int64_t>(b, (int64_t)c->smem_optin -
+                                       (int64_t)(sv[v].ring == 1   ? stream_smem_extra(L.jpad, sv[v].NW)
+                                                 : sv[v].ring == 2 ? mask_smem_extra(L.jpad, sv[v].NW)
+                                                                   : lane_smem_extra(L.jpad, sv[v].NW)));
         L.fold_words = (uint32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)pw, b / 4));
       }
       const double fw = budget > 0 ? std::min(pw, (double)L.fold_words) : 1.0;

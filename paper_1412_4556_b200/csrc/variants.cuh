@@ -35,7 +35,8 @@ struct StreamVariant {
   int NW;
   KernelFn fn, fn_olt;
   const char* name;
-  int ring;  // 0: per-lane queues (lane_kernel.cuh), 1: warp hit ring (stream_kernel.cuh)
+  int ring;  // 0: per-lane queues (lane_kernel.cuh), 1: warp hit ring (stream_kernel.cuh), 2: candidate masks
+             // (mask_kernel.cuh, trials of <= 1024 occurrences)
   int xs;    // 1: exact scan filter (lane_kernel.cuh XS)
 };
 const StreamVariant* stream_variants(int* n);  // kernels_stream.cu; first = default

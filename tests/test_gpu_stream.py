@@ -330,3 +330,49 @@ def test_fused_config_m_sampled(cuda_device):
     sample = np.arange(0, N, 60)
     want = oracle.ylt_for(cfg, elts, synth.make_yet_trials(cfg, sample))
     assert np.all(within_tol(fused[:, sample], want))
+
+
+# ------------------------------------------------------------------ candidate-mask kernel
+MASK_VARIANTS = (8, 9)  # ARA_OPT_STREAM - 1: mask kernel, 32 and 24 warps per block
+
+
+@pytest.mark.parametrize("K", [900, 1000, 1024])  # the mask kernel is built for 8 windows per trial
+def test_mask_kernel_bitwise(cuda_device, K):
+    """The candidate-mask kernel (trials of <= 1024 occurrences): integer regime bitwise vs the oracle for
+    every variant, incl. trials with more candidates than one staging chunk (dense layer), OLT, and its
+    fixed order (bitwise equal across launch shapes)."""
+    C, J = 20_000, 16
+    N = max(64, 600_000 // K // 10)
+    for n in (800, 8000):  # 8000 entries per ELT: ~100% of the rows present, > 256 candidates per trial
+        elts, layer, yet = _problem(J, C, n, K, N)
+        wy, wo = oracle.ylt_olt(C, yet, None, N, K, elts, [layer])
+        ctx = _ctx(C, elts, [layer])
+        for v in MASK_VARIANTS:
+            got = gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=v)
+            assert ctx.ara_kernel_name().startswith("ara_mask_kernel"), ctx.ara_kernel_name()
+            assert np.array_equal(got, wy), (K, n, v)
+        select(ctx, KERNEL_STREAM, MASK_VARIANTS[0])
+        ids = torch.from_numpy(yet.view(np.int32)).cuda()
+        y = torch.zeros((1, N), dtype=torch.float64, device=cuda_device)
+        o = torch.full((1, N), -1.0, dtype=torch.float64, device=cuda_device)
+        ctx.ara_run_ex(ids, y, o, events_per_trial=K, num_trials=N)
+        ctx.ara_check()
+        assert np.array_equal(y.cpu().numpy(), wy) and np.array_equal(o.cpu().numpy(), wo), (K, n)
+
+
+def test_mask_kernel_real_regime_and_invalid_ids(cuda_device):
+    C, J, K, N = 3_000_000, 16, 1000, 2000
+    elts, layer, yet = _problem(J, C, 20_000, K, N, integer=False, seed=5)
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx(C, elts, [layer])
+    ys = [gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=v) for v in MASK_VARIANTS]
+    assert np.array_equal(ys[0], ys[1])
+    assert np.all(within_tol(ys[0], want))
+    select(ctx, KERNEL_STREAM, MASK_VARIANTS[0])
+    for bad in (0, C + 1, 2**32 - 1):
+        b = yet.copy()
+        b[K * 77 + 5] = bad
+        with pytest.raises(ara.AraError) as e:
+            gpu_ylt(None, ctx, b, K=K, num_trials=N)
+        assert e.value.status == ara.ARA_E_RANGE
+    assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N), ys[0])
