@@ -224,8 +224,9 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           also marks YET ids evict_first), 1 no hints, 2 hints + persisting
  *                           access-policy window on the table
  *   ARA_OPT_PREFETCH        L2 prefetch of the YET ahead of the register-staged windows: -1 auto
- *                           (default: on for the fixed-length-trial kernels -- one bulk prefetch of the
- *                           trial after next per trial --, off for the presence kernel), 0 off, 1 on
+ *                           (default: on for the per-lane-queue and warp-ring kernels -- one bulk
+ *                           prefetch of the trial after next per trial --, off for the presence and
+ *                           candidate-mask kernels), 0 off, 1 on
  *                           (presence kernel: each warp prefetches its next trial at a trial start)
  *   ARA_OPT_VARIANT         kernel variant index within the selected kernel and row width
  *                           (ara_layer_info reports the count)
@@ -253,13 +254,17 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           with the option set) instead of the sparse records.  Bitwise identical
  *                           YLT; exact only for deterministic losses (no secondary uncertainty,
  *                           PAPER.md:125), and no ELT lookups happen at run time.
- *   ARA_OPT_STREAM          1 (default): for a YET of fixed-length trials (no offsets, K % 4 == 0, 16-B
- *                           aligned ids, catalogue < 2^32 - 2) the presence path runs a fixed-length-
- *                           trial kernel: v = 1..3 the per-lane-queue kernel (lane_kernel.cuh: each
- *                           lane queues the hits of its own window positions and sums them in stream
- *                           order; 32, 24, 16 warps per block; the default), v = 4 the warp-ring
- *                           kernel (stream_kernel.cuh: the presence kernel's summation order); 0 =
- *                           always the presence kernel.  Every kernel's order is fixed: the YLT is
+ *   ARA_OPT_STREAM          0 (default): the presence kernel.  v > 0: for a YET of fixed-length trials
+ *                           (no offsets, K % 4 == 0, 16-B aligned ids, catalogue < 2^32 - 2) the
+ *                           presence path runs a fixed-length-trial kernel instead: v = 1..3 the
+ *                           per-lane-queue kernel (lane_kernel.cuh: each lane queues the hits of its
+ *                           own window positions and sums them in stream order; 32, 24, 16 warps per
+ *                           block), v = 4 the warp-ring kernel (stream_kernel.cuh: the presence
+ *                           kernel's summation order), v = 5..8 the per-lane-queue kernel with the
+ *                           exact scan filter (see ARA_OPT_FILTER), v = 9, 10 the candidate-mask kernel
+ *                           (mask_kernel.cuh; 897 <= K <= 1024 only, else the presence kernel runs;
+ *                           10 adds a per-lane L2 prefetch four windows ahead).  Every kernel's order
+ *                           is fixed: the YLT is
  *                           reproducible bit for bit and independent of the sharding; across kernels it
  *                           agrees bitwise in the integer regime and to the rounding of the summation
  *                           order otherwise (amplified by FT3 when S_n is close to its retention).

@@ -5,6 +5,7 @@
 """
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -23,7 +24,8 @@ LIBS = {
     "libara_synth.so": [os.path.join(HERE, "synth", "synth.cu")],
 }
 DEPS = {
-    "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_kernel.cuh", "presence_kernel.cuh", "stream_kernel.cuh", "lane_kernel.cuh", "fused_kernel.cuh", "variants.cuh", "study.cuh", "common.cuh")] + [os.path.join(INCLUDE, "ara.h")],
+    # every header under csrc/ (a kernel header missing here once left a stale libara.so in place)
+    "libara.so": sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(INCLUDE, "ara.h")],
     "libara_synth.so": [os.path.join(INCLUDE, "ara_synth.h")],
 }
 OUT_DIR = {"libara.so": HERE, "libara_synth.so": os.path.join(HERE, "synth")}

@@ -484,7 +484,9 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
     // fixed-length trials: the stream kernel (stream_kernel.cuh), one block of NW warps per SM
     fn = olt ? svar->fn_olt : svar->fn;
     name = svar->name;
-    p.prefetch = c->prefetch != 0 ? 1u : 0u;  // auto: bulk L2 prefetch two trials ahead
+    // auto: bulk L2 prefetch two trials ahead (lane/ring kernels); the mask kernel: off (measured: the bulk
+    // prefetch doubles its DRAM bytes)
+    p.prefetch = c->prefetch < 0 ? (svar->ring == 2 ? 0u : 1u) : (c->prefetch != 0 ? 1u : 0u);
     threads = svar->NW * 32;
     int st_smem = 0;
     ara_status st = fn_static_smem(c, (const void*)fn, &st_smem);

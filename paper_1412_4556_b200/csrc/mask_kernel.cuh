@@ -75,7 +75,8 @@ __device__ __forceinline__ uint4 ld_ids4_keep(const uint32_t* p, uint64_t pol) {
 
 // NW: warps per block (one block per SM).  OLT: also the largest occurrence-net loss per trial.
 // NWIN: windows per trial (compile time; 8 covers K in (896, 1024], the paper's 1000 events per trial).
-template <int NW, bool OLT, int NWIN = 8>
+// PFD: > 0 = each lane also prefetches (prefetch.global.L2) its slots PFD windows ahead.
+template <int NW, bool OLT, int NWIN = 8, int PFD = 0>
 __global__ void __launch_bounds__(NW * 32, 1) ara_mask_kernel(const __grid_constant__ LayerParams p) {
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) uint32_t smem[];
@@ -100,61 +101,61 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_mask_kernel(const __grid_const
   const uint32_t nt = (uint32_t)(N > W ? (N - 1 - W) / NWT + 1 : 0);
   if (nt == 0) return;
   const uint32_t K = p.K;  // 4 .. 1024, multiple of 4
+  static_assert(NWIN >= 2, "the mask kernel needs at least two windows per trial");
   constexpr uint32_t nwin = NWIN;  // the host launches this kernel only when (K + 127) / 128 == NWIN
   const bool lane_last = 4u * lane < K - 128u * (nwin - 1u);
   const uint64_t pol_yet = make_policy(true, 1u);  // evict_last: the trial's lines stay for the reload
   const uint32_t C = p.C, fmul = p.fold_mul;
 
-  // ---- the staged trial: its candidates are issued as batches of 32 while the next trial is scanned
-  uint32_t st_total = 0;   // candidates of the staged trial
-  uint32_t st_chunk = 0;   // canonical index of staging[0] (chunks of kMaskStage)
-  uint32_t st_next = 0;    // next canonical index to issue
-  uint64_t st_t = 0;       // its trial index
-  uint32_t st_par = 0;     // its parity (accumulator)
-  bool st_live = false;    // a staged trial still has a batch to issue (an empty trial issues one empty batch)
-  bool st_pending = false; // the staged ids are still in flight (cp.async)
-  uint32_t st_mask = 0, st_prefix = 0;  // per lane: its candidate mask and exclusive prefix (chunk refills)
-  const uint32_t* st_ids = nullptr;     // per lane: its slots of the staged trial's first window
-  // ---- batches in flight (FIFO of <= 2, record slots alternate); each closes its trial if it is the last
-  uint32_t inflight = 0, slot_old = 0;
-  uint32_t f_par[2] = {0u, 0u}, f_last[2] = {0u, 0u};
-  uint64_t f_t[2] = {0u, 0u};
+  // ---- the previous trial's staged candidates (warp-uniform except S, M)
+  uint32_t pt_total = 0;   // candidates of the trial being consumed
+  uint32_t pt_chunk = 0;   // canonical index of staging[0] (chunks of kMaskStage)
+  uint32_t pt_next = 0;    // next canonical index to issue
+  uint64_t pt_t = 0;       // its trial index
+  bool pt_open = false;    // a trial is being consumed
+  uint32_t pt_mask = 0, pt_prefix = 0;  // per lane: its mask and exclusive prefix (for chunk refills)
+  const uint32_t* pt_ids = nullptr;     // per lane: its slots of the trial's first window (id reloads)
+  int inflight = 0;        // batches in flight (0..2)
+  uint32_t slot_old = 0;   // record slot of the oldest in-flight batch
   uint32_t vmax = 0;       // max over issued (id - 1); >= C marks an invalid id
-  double S0 = 0.0, S1 = 0.0, M0 = 0.0, M1 = 0.0;  // per lane: partial sums (and OLT maxima) by trial parity
+  double S = 0.0, Mx = 0.0;
 
-  // Stage candidates [st_chunk, st_chunk + kMaskStage) of the staged trial: every lane walks its set bits
-  // and cp.asyncs the ids whose canonical index falls in the chunk straight from global memory (L2) into
-  // the staging list (no register round trip); the next issue waits for them.
+  // Stage candidates [pt_chunk, pt_chunk + kMaskStage) of the trial being consumed: every lane walks its
+  // set bits and cp.asyncs the ids whose canonical index falls in the chunk straight from global memory
+  // (L2) into the staging list -- no register round trip; the first batch step waits for them.
+  bool staged_pending = false;
   auto stage_chunk = [&]() {
-    uint32_t m = st_mask, idx = st_prefix;
+    uint32_t m = pt_mask, idx = pt_prefix;
+    const uint32_t st_s = stage_s;
     while (m != 0u) {
-      const uint32_t bpos = __ffs(m) - 1u;
+      const uint32_t b = __ffs(m) - 1u;
       m &= m - 1u;
-      if (idx >= st_chunk && idx < st_chunk + kMaskStage)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(stage_s + 4u * (idx - st_chunk)),
-                     "l"(st_ids + (bpos >> 2) * 128u + (bpos & 3u))
+      if (idx >= pt_chunk && idx < pt_chunk + kMaskStage)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(st_s + 4u * (idx - pt_chunk)),
+                     "l"(pt_ids + (b >> 2) * 128u + (b & 3u))
                      : "memory");
       ++idx;
     }
     cp_async_commit();
-    st_pending = true;
+    staged_pending = true;
   };
-  auto close = [&](uint32_t par, uint64_t t) {  // fixed tree, FT3, one store (and the OLT maximum)
-    double v = par ? S1 : S0;
+  auto close = [&]() {  // fixed tree, FT3, one store (and the OLT maximum)
+    double v = S;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
-    if (lane == 0) p.ylt[t] = clamp_terms(v, p.r3, p.l3);  // step 4: FT3 on S_n
+    if (lane == 0) p.ylt[pt_t] = clamp_terms(v, p.r3, p.l3);
     if constexpr (OLT) {
-      double mm = par ? M1 : M0;
+      double mm = Mx;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) mm = fmax(mm, __shfl_xor_sync(FULL, mm, off));
-      if (lane == 0) p.olt[t] = mm;
-      if (par) M1 = 0.0; else M0 = 0.0;
+      if (lane == 0) p.olt[pt_t] = mm;
+      Mx = 0.0;
     }
-    if (par) S1 = 0.0; else S0 = 0.0;
+    S = 0.0;
+    pt_open = false;
   };
-  auto consume_oldest = [&]() {  // Steps 1-3 for the oldest batch in flight, accumulated by trial parity
-    if (inflight == 2u) asm volatile("cp.async.wait_group 1;" ::: "memory");
+  auto consume_oldest = [&]() {  // Steps 1-3 for the oldest batch in flight, accumulated per lane
+    if (inflight == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
     else cp_async_wait_all();
     const uint4 r = lds_u128(rec_l + slot_old * 512u);
     const uint32_t c1 = r.x & 0xffu, c2 = (r.x >> 8) & 0xffu, nz = (r.x >> 16) & 0xffu;
@@ -177,62 +178,61 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_mask_kernel(const __grid_const
       sum += clamp_fast((double)__uint_as_float(r.z), tb.x, tb.y);
     }
     const double o = clamp_fast(sum, p.r2, p.l2);  // step 3: FT2 (+0 for empty slots and zero rows)
-    const uint32_t par = slot_old ? f_par[1] : f_par[0];
-    S0 += par ? 0.0 : o;  // step 4 accumulation (x + 0 == x exactly)
-    S1 += par ? o : 0.0;
-    if constexpr (OLT) {
-      if (par) M1 = o > M1 ? o : M1;
-      else M0 = o > M0 ? o : M0;
-    }
-    if (slot_old ? f_last[1] : f_last[0]) close(par, slot_old ? f_t[1] : f_t[0]);
+    S += o;                                        // step 4 accumulation
+    if constexpr (OLT) Mx = o > Mx ? o : Mx;
     slot_old ^= 1u;
     --inflight;
   };
-  // Issue the staged trial's next batch of 32 (consuming the oldest batch first when both slots are busy).
-  auto issue = [&]() {
-    if (inflight == 2u) consume_oldest();
-    if (st_next >= st_chunk + kMaskStage) {  // more candidates than one staging chunk: refill (the batches of
-      __syncwarp();                         // the chunk already hold their records, not staging entries)
-      st_chunk += kMaskStage;
+  // One batch step: consume the oldest batch if both slots are busy, then issue the next 32 staged
+  // candidates (refilling the staging list when the chunk is used up).
+  auto batch_step = [&]() {
+    if (inflight == 2) consume_oldest();
+    if (pt_next >= pt_chunk + kMaskStage) {  // the trial has more candidates than one staging chunk
+      while (inflight) consume_oldest();       // the chunk's batches are done with the staging list
+      __syncwarp();
+      pt_chunk += kMaskStage;
       stage_chunk();
     }
-    if (st_pending) {  // the staged ids (the newest cp.async group; older record groups complete first anyway)
-      cp_async_wait_all();
+    if (staged_pending) {  // the staged ids have landed (no record batch is in flight here)
+      if (inflight == 0) cp_async_wait_all();
+      else asm volatile("cp.async.wait_group 1;" ::: "memory");
       __syncwarp();
-      st_pending = false;
+      staged_pending = false;
     }
-    const uint32_t i = st_next + lane;
-    const bool act = i < st_total;
-    uint32_t e = act ? lds_u32(stage_s + 4u * (i - st_chunk)) : 0u;
-    if (act) vmax = max(vmax, e - 1u);  // an invalid id reached the list via the sentinel (0 wraps)
-    e = min(e, C + 1u);                  // invalid ids read the all-zero record C + 1
-    const uint32_t slot = slot_old ^ inflight;
+    const uint32_t i = pt_next + lane;
+    const bool act = i < pt_total;
+    uint32_t e = act ? lds_u32(stage_s + 4u * (i - pt_chunk)) : 0u;
+    vmax = act ? max(vmax, e - 1u) : vmax;  // an invalid id reached the list via the sentinel (0 wraps)
+    e = min(e, C + 1u);                        // invalid ids read the all-zero record C + 1
+    const uint32_t slot = slot_old ^ (uint32_t)inflight;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(rec_l + slot * 512u), "l"(p.rec + e),
                  "r"(act ? 16u : 0u)
                  : "memory");
     cp_async_commit();
-    st_next += 32u;
-    const uint32_t last = st_next >= st_total ? 1u : 0u;
-    if (slot) {
-      f_par[1] = st_par; f_last[1] = last; f_t[1] = st_t;
-    } else {
-      f_par[0] = st_par; f_last[0] = last; f_t[0] = st_t;
-    }
-    st_live = !last;
     ++inflight;
+    pt_next += 32u;
+  };
+  // Finish the trial being consumed: every remaining batch, then close it.
+  auto finish = [&]() {
+    if (!pt_open) return;
+    while (pt_next < pt_total) batch_step();
+    while (inflight) consume_oldest();
+    if (staged_pending) {  // a trial without candidates: its (empty) staging group
+      cp_async_wait_all();
+      staged_pending = false;
+    }
+    __syncwarp();  // every lane is done with the staging list before it is refilled
+    close();
   };
 
   const uint64_t tstride = NWT * K;
   const uint32_t* lp = p.ids + W * K + 4u * lane;  // this lane's slots of the trial's first window
-  // window w + 1 (or the next trial's window 0) is requested while window w is tested.  A look-ahead of
-  // two windows (three rotating register sets) measured no faster (1.392 vs 1.39 ms on P) and spills at
-  // NW = 32, so one window it is
   uint4 A = make_uint4(0u, 0u, 0u, 0u);
   if (nwin > 1u || lane_last) A = ld_ids4_keep(lp, pol_yet);
   for (uint32_t k = 0; k < nt; ++k) {
     if (p.prefetch && lane == 0 && k + 2u < nt) prefetch_l2_bulk(lp + 2u * tstride - 4u * lane, K * 4u);
     uint32_t mask = 0;
-    // ---- scan the trial: one presence test and one predicated OR per id; a batch step of the staged
+    // ---- scan the trial: one presence test and one predicated OR per id; a batch step of the previous
     // trial after every second window
     auto window = [&](auto wc) {
       constexpr uint32_t w = decltype(wc)::value;
@@ -241,12 +241,17 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_mask_kernel(const __grid_const
       if constexpr (!last) {
         if (w + 2u < nwin || lane_last) nxt = ld_ids4_keep(lp + 128u * (w + 1u), pol_yet);
       } else {
-        if (k + 1u < nt && (nwin > 1u || lane_last)) nxt = ld_ids4_keep(lp + tstride, pol_yet);
+        if (k + 1u < nt && (nwin > 1u || lane_last)) nxt = ld_ids4_keep(lp + tstride, pol_yet);  // next trial
+      }
+      if constexpr (PFD > 0) {  // per-lane L2 prefetch PFD windows ahead (into the next trial)
+        constexpr uint32_t g = w + (uint32_t)PFD;
+        const uint32_t* pf = g < nwin ? lp + 128u * g : lp + tstride + 128u * (g - nwin);
+        if (g < nwin || k + 1u < nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
       }
       test_mark4<(int)w>(A, C, fmul, bits_s, (!last || lane_last) ? 0xffffffffu : 0u, mask);
       A = nxt;
-      if constexpr ((w & 1u) == 1u) {
-        if (st_live) issue();
+      if constexpr ((w & 1u) == 0u) {
+        if (pt_open && pt_next < pt_total) batch_step();
       }
     };
     window(std::integral_constant<uint32_t, 0>{});
@@ -257,8 +262,8 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_mask_kernel(const __grid_const
     if constexpr (nwin > 5) window(std::integral_constant<uint32_t, 5>{});
     if constexpr (nwin > 6) window(std::integral_constant<uint32_t, 6>{});
     if constexpr (nwin > 7) window(std::integral_constant<uint32_t, 7>{});
-    // ---- every batch of the staged trial is issued (its records are in flight); stage this trial
-    while (st_live) issue();
+    // ---- the previous trial is done: close it; then stage this trial's candidates
+    finish();
     const uint32_t cnt = __popc(mask);
     uint32_t incl = cnt;
 #pragma unroll
@@ -266,21 +271,18 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_mask_kernel(const __grid_const
       const uint32_t y = __shfl_up_sync(FULL, incl, off);
       if (lane >= (uint32_t)off) incl += y;
     }
-    __syncwarp();  // every lane has read the staging list of the previous trial
-    st_total = __shfl_sync(FULL, incl, 31);
-    st_prefix = incl - cnt;
-    st_mask = mask;
-    st_ids = lp;
-    st_t = W + (uint64_t)k * NWT;
-    st_par = k & 1u;
-    st_chunk = 0;
-    st_next = 0;
-    st_live = true;  // a trial without candidates still issues one (empty) batch that closes it
+    pt_total = __shfl_sync(FULL, incl, 31);
+    pt_prefix = incl - cnt;
+    pt_mask = mask;
+    pt_ids = lp;
+    pt_t = W + (uint64_t)k * NWT;
+    pt_chunk = 0;
+    pt_next = 0;
+    pt_open = true;
     stage_chunk();
     lp += tstride;
   }
-  while (st_live) issue();
-  while (inflight) consume_oldest();
+  finish();
   const bool bad = __any_sync(FULL, vmax >= C);
   if (lane == 0 && bad) atomicOr(p.err, 1u);
 }

@@ -81,7 +81,7 @@ def within_tol(gpu, ref, rel=1e-6, abs_floor=1e-3):
 
 
 KERNEL_STREAM = 2       # test-level selector: the presence path with the fixed-length stream kernel
-STREAM_VARIANTS = 10    # ARA_OPT_STREAM = 1..10 (lane 32/24/16; ring; lane XS 24, XS2 24, XS 32/16; mask 32/24)
+STREAM_VARIANTS = 10    # ARA_OPT_STREAM = 1..10 (lane 32/24/16; ring; lane XS 24, XS2 24, XS 32/16; mask, mask + L2 prefetch)
 
 
 def select(ctx, kernel, variant=0):

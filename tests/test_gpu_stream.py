@@ -333,7 +333,7 @@ def test_fused_config_m_sampled(cuda_device):
 
 
 # ------------------------------------------------------------------ candidate-mask kernel
-MASK_VARIANTS = (8, 9)  # ARA_OPT_STREAM - 1: mask kernel, 32 and 24 warps per block
+MASK_VARIANTS = (8, 9)  # ARA_OPT_STREAM - 1: mask kernel without / with the per-lane L2 prefetch
 
 
 @pytest.mark.parametrize("K", [900, 1000, 1024])  # the mask kernel is built for 8 windows per trial
