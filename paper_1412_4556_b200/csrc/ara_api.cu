@@ -78,6 +78,8 @@ struct Layer {
   uint32_t fold_words = 0;  // canonical fold size of this layer (every presence/stream launch uses it)
   bool xs_auto = false;     // fixed-length trials: the exact scan filter pays (ARA_OPT_FILTER auto)
   uint4* rec = nullptr;         // sparse row records (C + 2) x 16 B; record C + 1 is all zero (invalid ids)
+  uint2* xrank = nullptr;       // XS, built on first use: per bitmap word (word, loss-holding rows before it)
+  uint4* rec_c = nullptr;       // XS: records of the loss-holding rows only (+ one zero record)
   double* occ = nullptr;        // precombined o[e] per event, (C + 1) x 8 B, built on first use
   // Section IV.B study structures, built on first use by ara_run_study
   float* indep = nullptr;         // J x (C + 1) independent per-ELT direct-access arrays
@@ -260,6 +262,66 @@ __global__ void __launch_bounds__(256) record_build_kernel(uint4* __restrict__ r
   }
 }
 
+// XS compact-row index (the event -> compact row map of SURVEY N2, folded into the exact
+// scan filter).  Block b of 1024 words: bsum[b] = rows holding a loss in it.
+__global__ void __launch_bounds__(1024) rank_count_kernel(const uint32_t* __restrict__ present, uint32_t words,
+                                                          uint32_t* __restrict__ bsum) {
+  const uint32_t w = blockIdx.x * 1024u + threadIdx.x;
+  uint32_t v = w < words ? __popc(present[w]) : 0u;
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __shared__ uint32_t ws[32];
+  if ((threadIdx.x & 31u) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int i = 0; i < 32; ++i) t += ws[i];
+    bsum[blockIdx.x] = t;
+  }
+}
+// Exclusive prefix of the block sums (one thread: a few hundred blocks, built once per layer).
+__global__ void rank_scan_kernel(uint32_t* bsum, uint32_t nb) {
+  uint32_t t = 0;
+  for (uint32_t b = 0; b < nb; ++b) {
+    const uint32_t v = bsum[b];
+    bsum[b] = t;
+    t += v;
+  }
+}
+// xrank[w] = (word w, loss-holding rows in words < w); then each loss-holding row's record is copied to
+// its rank: rec_c[rank(e)] = rec[e].
+// Entries run through word (C + 1) >> 5 (`xwords`), where bit C + 1 -- no row, rank = every row holding a
+// loss -- is set: an invalid id (x = C after the clamp) is an exact hit on the zero record.
+__global__ void __launch_bounds__(1024) rank_write_kernel(const uint32_t* __restrict__ present, uint32_t words,
+                                                          uint32_t xwords, uint32_t C,
+                                                          const uint32_t* __restrict__ bsum, const uint4* __restrict__ rec,
+                                                          uint2* __restrict__ xrank, uint4* __restrict__ rec_c) {
+  const uint32_t w = blockIdx.x * 1024u + threadIdx.x, lane = threadIdx.x & 31u;
+  const uint32_t word = w < words ? present[w] : 0u;
+  const uint32_t c = __popc(word);
+  uint32_t incl = c;
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= (uint32_t)off) incl += y;
+  }
+  __shared__ uint32_t ws[32];
+  if (lane == 31u) ws[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  if (threadIdx.x < 32u) {
+    uint32_t v = ws[threadIdx.x], x = v;
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+      if (threadIdx.x >= (uint32_t)off) x += y;
+    }
+    ws[threadIdx.x] = x - v;  // exclusive over the block's warps
+  }
+  __syncthreads();
+  if (w >= xwords) return;
+  uint32_t base = bsum[blockIdx.x] + ws[threadIdx.x >> 5] + incl - c;
+  const uint32_t sentinel = w == (C + 1u) >> 5 ? 1u << ((C + 1u) & 31u) : 0u;
+  xrank[w] = make_uint2(word | sentinel, base);
+  for (uint32_t m = word; m != 0u; m &= m - 1u) rec_c[base++] = rec[(uint64_t)w * 32u + (__ffs(m) - 1u)];
+}
+
 // the union presence bitmap of a layer group (word-wise OR of the layers' bitmaps).
 __global__ void __launch_bounds__(256) union_bitmap_kernel(uint32_t* __restrict__ out, const uint32_t* const* in,
                                                            uint32_t nl, uint32_t words) {
@@ -324,6 +386,8 @@ static void destroy_ctx(ara_ctx* c) {
     cudaFree(L.present);
     for (auto& f : L.folds) cudaFree(f.buf);
     cudaFree(L.rec);
+    cudaFree(L.xrank);
+    cudaFree(L.rec_c);
     cudaFree(L.occ);
     cudaFree(L.indep);
     cudaFree(L.sorted_ids);
@@ -428,6 +492,31 @@ static ara_status get_fold(ara_ctx* c, Layer& L, uint32_t words, cudaStream_t st
   return ARA_OK;
 }
 
+// The XS compact-row index of a layer (built on first use, stream-ordered, never rebuilt).
+static ara_status get_compact(ara_ctx* c, Layer& L, cudaStream_t stream) {
+  if (L.xrank) return ARA_OK;
+  const uint32_t words = L.present_words, xwords = (uint32_t)((c->C + 1ull) >> 5) + 1u;
+  const uint32_t nb = (std::max(words, xwords) + 1023u) / 1024u;
+  uint32_t* bsum = nullptr;
+  if (cudaMalloc(&L.xrank, (size_t)xwords * sizeof(uint2)) != cudaSuccess ||
+      cudaMalloc(&L.rec_c, (L.present_rows + 1) * sizeof(uint4)) != cudaSuccess ||
+      cudaMallocAsync((void**)&bsum, (size_t)nb * 4, stream) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(L.xrank);
+    cudaFree(L.rec_c);
+    L.xrank = nullptr;
+    L.rec_c = nullptr;
+    return set_error(ARA_E_NOMEM, "compact-row index");
+  }
+  ARA_CUDA(cudaMemsetAsync(L.rec_c + L.present_rows, 0, sizeof(uint4), stream));  // the zero record
+  rank_count_kernel<<<nb, 1024, 0, stream>>>(L.present, words, bsum);
+  rank_scan_kernel<<<1, 1, 0, stream>>>(bsum, nb);
+  rank_write_kernel<<<nb, 1024, 0, stream>>>(L.present, words, xwords, c->C, bsum, L.rec, L.xrank, L.rec_c);
+  ARA_CUDA(cudaGetLastError());
+  cudaFreeAsync(bsum, stream);
+  return ARA_OK;
+}
+
 // The fixed-length-trial kernel applies to a YET of fixed length K (K % 4 == 0, 16-B aligned ids), a
 // catalogue below 2^32 - 2 and per-warp hit ordinals that cannot wrap.
 static bool stream_eligible(const ara_ctx* c, const uint32_t* ids, const uint64_t* offsets, uint64_t num_trials,
@@ -501,6 +590,13 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
     const uint32_t fw = (uint32_t)std::min<int64_t>(L.fold_words, budget / 4);
     st = get_fold(c, L, fw, stream, &fold, &mul);
     if (st) return st;
+    if (svar->xs) {
+      st = get_compact(c, L, stream);
+      if (st) return st;
+      p.xrank = L.xrank;
+      p.rec_c = L.rec_c;
+      p.rec_zero = (uint32_t)L.present_rows;
+    }
     p.present = fold;
     p.rec = L.rec;
     p.exact = L.present;

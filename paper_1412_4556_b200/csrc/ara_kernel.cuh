@@ -49,6 +49,11 @@ struct LayerParams {
   uint32_t fold_mul;         // 2^27 (no folding: word x >> 5) or floor((present_words * 2^32 - 1) / C)
   const uint4* rec;          // per-event sparse row record (presence kernels with one lane per row)
   const uint32_t* exact;     // UNFOLDED presence bitmap (bit e of word e >> 5), for the FX filter stage
+  const uint2* xrank;        // XS: per word of the unfolded bitmap (the word, rows with a loss before it),
+                             // through the word of bit C + 1, which is set there (the invalid-id sentinel)
+  const uint4* rec_c;        // XS: the sparse records of the rows holding a loss only, in row order (rank
+                             // = index), then one all-zero record at index rec_zero (invalid ids)
+  uint32_t rec_zero;         // XS: rows holding a loss
   const double* occ;         // precombined occurrence-net loss FT2(sum_j FT1(l_ej)) per event
   uint32_t round_min;        // lane kernel: lanes with a queued hit that trigger a gather round
   uint32_t interleave;       // fixed-length kernels: 1 = trials interleaved over the grid's warps, 0 = blocks

@@ -66,11 +66,15 @@ __device__ __forceinline__ void test_enqueue(uint32_t id, uint32_t C, uint32_t f
 }
 
 // XS (exact scan filter, for catalogues far larger than the shared bitmap, config X): the folded test
-// only nominates CANDIDATES; each candidate loads the word of the layer's unfolded presence bitmap
-// (global memory, L2-resident, bit e = row e holds a loss) that decides it exactly.  The load is issued
-// while scanning window w and used one window later, where only exact hits (and invalid ids, forced
-// through) enter the lane's queue.  A false positive then costs one L2 word instead of a queue slot, a
-// gather round and a record fetch; the queue order -- hence the YLT bits -- is unchanged.
+// only nominates CANDIDATES; each candidate loads the rank entry of its word of the layer's unfolded
+// presence bitmap (global memory, L2-resident: the word, bit e = row e holds a loss, and the number of
+// rows holding a loss before it) that decides it exactly.  The load is issued while scanning window w and
+// used one window later, where only exact hits (and invalid ids, forced through) enter the lane's queue
+// -- as their COMPACT record index, the rank of the row among the rows that hold a loss (the event ->
+// compact-row index of PAPER.md:211-213's direct-access table without its zero rows).  A false positive
+// costs one L2 entry instead of a queue slot, a gather round and a record fetch, and the records a hit
+// fetches form a table of the loss-holding rows only (15 MB for config X instead of 160 MB: L2-resident).
+// The queue order and the records -- hence the YLT bits -- are those of the plain path.
 __device__ __forceinline__ uint32_t fold_candidate(uint32_t id, uint32_t C, uint32_t fmul, uint32_t bits_s,
                                                    uint32_t valid, uint32_t& x) {
   x = min(id - 1u, C);
@@ -78,21 +82,25 @@ __device__ __forceinline__ uint32_t fold_candidate(uint32_t id, uint32_t C, uint
   return (w >> (x & 31u)) & valid & 1u;
 }
 
-// Append x to the lane's queue when bit (x + 1) & 31 of the exact word is set.
-__device__ __forceinline__ void exact_enqueue(uint32_t ew, uint32_t x, uint32_t q_l, uint32_t& tail) {
+// When bit s = (x + 1) & 31 of the exact word ew.x is set, append the row's compact record index
+// ew.y + popc(ew.x & (2^s - 1)) to the lane's queue.
+__device__ __forceinline__ void exact_enqueue(uint2 ew, uint32_t x, uint32_t q_l, uint32_t& tail) {
   asm volatile(
       "{\n"
       " .reg .pred p;\n"
-      " .reg .b32 s, m, a;\n"
-      " add.u32 s, %1, 1;\n and.b32 s, s, 31;\n shl.b32 m, 1, s;\n and.b32 m, m, %2;\n setp.ne.b32 p, m, 0;\n"
-      " and.b32 a, %0, 0x380;\n or.b32 a, a, %3;\n"
-      " @p st.shared.u32 [a], %1;\n"
+      " .reg .b32 s, m, h, r, a;\n"
+      " add.u32 s, %1, 1;\n and.b32 s, s, 31;\n shl.b32 m, 1, s;\n and.b32 h, m, %2;\n setp.ne.b32 p, h, 0;\n"
+      " sub.u32 m, m, 1;\n and.b32 m, m, %2;\n popc.b32 r, m;\n add.u32 r, r, %3;\n"
+      " and.b32 a, %0, 0x380;\n or.b32 a, a, %4;\n"
+      " @p st.shared.u32 [a], r;\n"
       " @p add.u32 %0, %0, 128;\n"
       "}\n"
       : "+r"(tail)
-      : "r"(x), "r"(ew), "r"(q_l)
+      : "r"(x), "r"(ew.x), "r"(ew.y), "r"(q_l)
       : "memory");
 }
+
+
 
 // NW: warps per block (one block per SM).  OLT: also the largest occurrence-net loss per trial.
 // XS: exact scan filter (see exact_enqueue).
@@ -144,6 +152,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
   uint32_t tail = 0, head = 0;
   uint32_t pb = 0;        // queued entries (at the head) that belong to the PREVIOUS trial
   uint32_t bx = 0;        // in-flight round: this lane's x = id - 1 (C: invalid), for rows read in full
+                          // (XS: its compact record index)
   uint32_t bpar = 0;      // its trial parity
   uint32_t vmax = 0;      // max over popped x; x == C marks an invalid id
   bool inflight = false;  // a round's records are in flight (warp-uniform)
@@ -161,7 +170,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
     double sum = 0.0;
     if (__any_sync(FULL, nz > 2u)) {  // rare: a row with more than two losses is read in full
       if (nz > 2u) {
-        const float* row = p.table + (uint64_t)(bx + 1u) * jpad;
+        const float* row = p.table + (uint64_t)(XS ? r.w : bx + 1u) * jpad;  // r.w: the row's event id
         for (uint32_t j = 0; j < jpad; ++j) {
           const float x = row[j];
           if (x != 0.0f) {
@@ -196,11 +205,16 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
     if (act) {
       head += 128u;
       pb -= isprev ? 1u : 0u;
-      vmax = max(vmax, x);
+      vmax = max(vmax, x);  // XS: x is a compact record index, rec_zero only for an invalid id
     }
-    bx = act ? x : C;
     bact = act;
-    cp_async16_zf(rec_l, p.rec + (bx + 1u), act ? 16u : 0u);  // x + 1 = the id; C + 1: the zero record
+    if constexpr (XS) {  // x: the compact record index (rec_zero: the zero record)
+      bx = act ? x : p.rec_zero;
+      cp_async16_zf(rec_l, p.rec_c + bx, act ? 16u : 0u);
+    } else {
+      bx = act ? x : C;
+      cp_async16_zf(rec_l, p.rec + (bx + 1u), act ? 16u : 0u);  // x + 1 = the id; C + 1: the zero record
+    }
     cp_async_commit();
     inflight = true;
   };
@@ -222,11 +236,19 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
   // Scan one window: presence test per id, hits appended to the lane's own queue.
   // XS: the previous window's candidates (x, exact word; a non-candidate holds word 0); with XD == 2 also
   // the window before it (qx*, qw*), tested first
-  uint32_t px0 = 0, px1 = 0, px2 = 0, px3 = 0, pw0 = 0, pw1 = 0, pw2 = 0, pw3 = 0;
-  uint32_t qx0 = 0, qx1 = 0, qx2 = 0, qx3 = 0, qw0 = 0, qw1 = 0, qw2 = 0, qw3 = 0;
-  auto exact_load = [&](uint32_t cand, uint32_t x) -> uint32_t {
-    uint32_t w = 0u;
-    if (cand) w = x < C ? ld_id(p.exact + ((x + 1u) >> 5), pol_exact) : 0xffffffffu;  // invalid: forced hit
+  const uint2 z2 = make_uint2(0u, 0u);
+  uint32_t px0 = 0, px1 = 0, px2 = 0, px3 = 0, qx0 = 0, qx1 = 0, qx2 = 0, qx3 = 0;
+  uint2 pw0 = z2, pw1 = z2, pw2 = z2, pw3 = z2, qw0 = z2, qw1 = z2, qw2 = z2, qw3 = z2;
+  // a candidate's rank entry: word (x + 1) >> 5; an invalid id (x = C) reads the sentinel bit C + 1,
+  // whose rank is rec_zero (no row holding a loss lies after it).  Predicated, no branch.
+  const uint2* const xr = p.xrank;
+  auto exact_load = [&](uint32_t cand, uint32_t x) -> uint2 {
+    uint2 w = z2;
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n"
+        " @q ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%3], %4;\n}\n"
+        : "+r"(w.x), "+r"(w.y)
+        : "r"(cand), "l"(xr + ((x + 1u) >> 5)), "l"(pol_exact));
     return w;
   };
   auto flush_oldest = [&]() {  // XS: the oldest pending window's exact hits enter the queue (slot order)
@@ -243,7 +265,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
       exact_enqueue(pw2, px2, q_l, tail);
       exact_enqueue(pw3, px3, q_l, tail);
     }
-    pw0 = pw1 = pw2 = pw3 = 0u;
+    pw0 = pw1 = pw2 = pw3 = z2;
   };
   auto flush_pending = [&]() {  // XS: every pending window, oldest first
     flush_oldest();
@@ -314,7 +336,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
   consume();
   if (nt >= 2u) close((nt - 2u) & 1u, nt - 2u);
   close((nt - 1u) & 1u, nt - 1u);
-  const bool bad = __any_sync(FULL, vmax >= C);
+  const bool bad = __any_sync(FULL, vmax >= (XS ? p.rec_zero : C));
   if (lane == 0 && bad) atomicOr(p.err, 1u);
 }
 

@@ -228,6 +228,38 @@ def test_exact_scan_filter_stress_shape(cuda_device):
         gpu_ylt(None, ctx, b, K=K, num_trials=N)
 
 
+def test_exact_scan_filter_compact_records_dense(cuda_device):
+    """The exact scan filter's compact-row index (rank over the unfolded bitmap, records of the
+    loss-holding rows only) on a small, dense catalogue: rows with 1..8 losses (rows with > 2 read in
+    full via the record's event id), loss-holding rows at every position of a bitmap word (ids 31, 32,
+    63, 64, ...), the last row C, and invalid ids reported.  Every XS variant equals the oracle bitwise
+    (integer regime) and the plain lane kernel."""
+    C, J, K, N = 4099, 8, 256, 600
+    rng = np.random.default_rng(23)
+    elts = []
+    for j in range(J):
+        ids = np.unique(np.concatenate([rng.integers(1, C + 1, size=900), [31, 32, 63, 64, 1, C]]))
+        rng.shuffle(ids)
+        losses = rng.integers(1, 1 << 20, size=ids.size)
+        elts.append((ids.astype(np.uint32), losses.astype(np.float32), (float(rng.integers(0, 1 << 12)), float(1 << 21))))
+    layer = (list(range(J)), (3000.0, float(1 << 24)), (1e5, 4e7))
+    yet = rng.integers(1, C + 1, size=N * K).astype(np.uint32)
+    yet[:8] = [31, 32, 63, 64, 1, C, 33, 62]
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx(C, elts, [layer])
+    for v in (4, 5, 6, 7):  # XS 24, XS2 24, XS 32/16 warps
+        got = gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=v)
+        assert ",XS" in ctx.ara_kernel_name(), ctx.ara_kernel_name()
+        assert np.array_equal(got, want), v
+    assert np.array_equal(gpu_ylt(None, ctx, yet, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=0), want)
+    for bad in (C + 1, 0, 0xFFFFFFFF):
+        b = yet.copy()
+        b[K * 5 + 77] = bad
+        with pytest.raises(ara.AraError):
+            gpu_ylt(None, ctx, b, K=K, num_trials=N, kernel=KERNEL_STREAM, variant=4)
+    ctx.close()
+
+
 def test_exact_scan_filter_config_x_sampled(cuda_device):
     """Config X itself (real regime) on a 20,000-trial slice generated on the device: the automatic
     kernel (lane + exact scan filter) within tolerance of the oracle on 500 sampled trials and of the
