@@ -1104,7 +1104,7 @@ static ara_status plan_step(ara_ctx* c, const ara_yet* yet, double* ylt, const d
   if (st) return st;
   for (size_t l = 0; m && l < c->layers.size(); ++l) {
     st = metrics_device_into(ylt + l * yet->num_trials, yet->num_trials, rps, m, pml_dev ? pml_dev + l * m : nullptr,
-                             tvar_dev ? tvar_dev + l * m : nullptr, scratch, bytes, s);
+                             tvar_dev ? tvar_dev + l * m : nullptr, scratch, bytes, s, true);
     if (st) return st;
   }
   return ARA_OK;
@@ -1141,6 +1141,11 @@ ara_status ara_plan_create(ara_ctx* c, const ara_yet* yet, double* ylt, const do
     cudaGetLastError();
     plan_free(p);
     return set_error(ARA_E_NOMEM, "metric scratch");
+  }
+  // zeroed once: the metric launches leave their scratch as they found it (metrics.cu, metrics_select)
+  if (bytes && cudaMemset(p->scratch, 0, bytes) != cudaSuccess) {
+    plan_free(p);
+    return cuda_error(cudaGetLastError(), "metric scratch");
   }
   // one eager step first: builds the folds and caches every launch attribute, so the capture records
   // stream work only (and validates the arguments)

@@ -14,7 +14,7 @@ ara_status cuda_error(cudaError_t e, const char* what);
 // metrics.cu: PML/TVaR into caller-provided device scratch (no allocation, graph-capturable)
 size_t metrics_scratch_size(uint64_t n);
 ara_status metrics_device_into(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
-                               double* tvar_dev, char* scratch, size_t bytes, cudaStream_t s);
+                               double* tvar_dev, char* scratch, size_t bytes, cudaStream_t s, bool zeroed);
 
 // Restores the caller's current device on scope exit.
 struct DeviceGuard {

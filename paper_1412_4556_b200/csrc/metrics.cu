@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -227,263 +228,577 @@ __global__ void __launch_bounds__(kSelBlock) tail_pass(const double* __restrict_
 }
 
 // ------------------------------------------------------------------------------------------------
-// Fused variant: ONE cooperative launch runs the 8 radix passes and the tail pass, separated by grid
-// barriers.  Each block keeps its contiguous chunk of keys in shared memory (when it fits), so the
-// YLT is read from HBM once; every block redundantly derives the per-query digits from the final
-// global histogram of the pass (triple-buffered so it can be cleared two passes ahead).
-constexpr int kFusedBlock = 1024;   // one block per SM: fewer arrivals at each grid barrier
-constexpr int kCacheKeys = 8192;    // 64 KB of cached keys per block (N <= 1.2M on 148 SMs)
+// metrics_select: ONE cooperative launch (one 1024-thread block per SM) selects every query's k-th
+// largest key with as few grid barriers as the data allow (typically 3; at most 6):
+//
+//   A  every block caches its contiguous chunk of keys in shared memory and histograms the top 16 bits
+//      (65,536 u16 bins in shared memory; a 256-bin coarse histogram beside the fine one in global
+//      memory), and publishes its chunk's largest and smallest key with their multiplicities;
+//      -- barrier --  a query whose rank falls on the global maximum (or minimum) key is DONE (T = that
+//      key: the tie block of capped or zero years, reading c14); every other query finds its 16-bit
+//      bucket (coarse, then fine bins) and its rank inside it;
+//   H  while a query's bucket holds more than kCandCap keys: histogram the next 12 bits of the keys of
+//      each such bucket (distinct buckets share nothing; queries in one bucket share its histogram)
+//      -- barrier --  narrow (coarse 64 + fine 64 bins); a full 64-bit prefix is the key itself (DONE);
+//   C  every bucket of <= kCandCap keys is COMPACTED into a global candidate list, and every block sums,
+//      per query, the values above the query's bucket (or above T) in a fixed order -- barrier --;
+//   F  block 0 sorts each candidate list (rank counting: at most kCandCap keys), reads T = the rank's
+//      key, and TVaR = (sum above T + (k - count above T) * T) / k with the block partials combined in
+//      block order, then the candidates above T in descending order -- bitwise reproducible.
+//
+// The global histograms of passes H live in scratch that every launch zeroes during pass A; pass A's
+// own histogram is zeroed by the launch that used it, after its last reader (the scratch is zeroed once
+// when it is allocated).  Barrier state is self-resetting.
+constexpr int kSelThreads = 1024;
+constexpr uint32_t kSelCache = 8192;      // cached keys per block (64 KB): n <= 8192 * SMs is read once
+constexpr uint32_t kSelHistWords = 32768; // 128 KB of packed u16 bin counters
+constexpr uint32_t kSelSub = 65535;       // keys per histogram sub-chunk (a u16 counter cannot overflow)
+constexpr uint32_t kCandCap = 256;        // bucket size compacted instead of narrowed further
+constexpr int kSelMaxBlocks = 256;
+constexpr int kSelHPasses = 4;            // 16 + 4 x 12 = 64 bits
+enum : int { kModeHist = 0, kModeCand = 1, kModeDone = 2 };
 
-struct FusedState {  // zeroed (cudaMemsetAsync) before every launch
-  unsigned int H[3][kMaxQ][256];
-  unsigned int bar_count, bar_gen;
+struct alignas(16) SelScratch {  // global scratch of metrics_select (zeroed once at allocation)
+  unsigned bar_count, bar_exit;
+  unsigned long long trace[kSelMaxBlocks][24];  // ARA_METRICS_TRACE: every block's %globaltimer at phase boundaries
+  unsigned cand_n[kMaxQ];
+  unsigned long long bmax[kSelMaxBlocks], bmin[kSelMaxBlocks];
+  unsigned bcmax[kSelMaxBlocks], bcmin[kSelMaxBlocks];
+  unsigned long long cand[kMaxQ][kCandCap];
+  double psum[kSelMaxBlocks][kMaxQ];
+  alignas(16) unsigned HA_c[256];
+  alignas(16) unsigned HA_f[65536];
+  alignas(16) unsigned HB_c[kSelHPasses][kMaxQ][64];
+  alignas(16) unsigned HB_f[kSelHPasses][kMaxQ][4096];
 };
 
-struct FusedQueries {  // kernel parameter
+struct SelQueries {  // kernel parameter
   uint64_t k[kMaxQ];
 };
 
-__device__ __forceinline__ void grid_sync(unsigned int* count, unsigned int* gen, unsigned int nb) {
+// Grid barrier: arrival by a release reduction, polling by acquire loads of a counter that only grows
+// during a launch (barrier i waits for i * gridDim.x arrivals); the last block past the final barrier
+// resets it.  Measured on B200 (148 x 1024 threads): ~1.3 us per barrier, vs ~2.3 us for a fence +
+// atomic + generation-flag barrier.
+__device__ __forceinline__ void grid_sync(unsigned int* count, unsigned int target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = gen;
-    const unsigned int g = *vgen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == nb - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (*vgen == g) __nanosleep(32);
-    }
-    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while ((int)(v - target) < 0);
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kFusedBlock) metrics_fused(const double* __restrict__ y, uint64_t n, int m,
-                                                              FusedState* st, double* __restrict__ psum,
-                                                              unsigned long long* __restrict__ pcnt,
-                                                              const __grid_constant__ FusedQueries Q,
-                                                              double* __restrict__ pml_out, double* __restrict__ tvar_out) {
-  extern __shared__ uint64_t skeys[];
-  __shared__ unsigned int sh[kMaxQ][256];
-  __shared__ uint64_t s_prefix[kMaxQ], s_rank[kMaxQ], s_slot_prefix[kMaxQ];
-  __shared__ int s_q2slot[kMaxQ], s_nslot;
-  __shared__ double wsum[kFusedBlock / 32][kMaxQ];
-  __shared__ unsigned long long wcnt[kFusedBlock / 32][kMaxQ];
-  __shared__ uint32_t s_nact, s_nnext;
-  // ACTIVE key lists (cached case): after a pass only the keys that fed some slot's histogram can
-  // matter to the next passes, so each pass scans the previous pass's survivors only (indices into the
-  // cached keys; the tail still reads every key)
-  const uint32_t act_s = (uint32_t)__cvta_generic_to_shared(skeys + kCacheKeys);  // two u16 lists of kCacheKeys
+// Warp: the digit d of the bucket holding rank r (1-based from the top) of a histogram of 32*PER bins
+// in global memory (h[0] = digit 0), and the count of keys in larger digits.  Lane l owns the bins
+// 32*PER-1-PER*l .. 32*PER-PER*l (descending).  Requires r <= the histogram's total.
+template <int PER, bool SHARED = false>
+__device__ __forceinline__ void find_digit(const unsigned* h, uint32_t r, int lane, uint32_t& d, uint32_t& above) {
+  constexpr int NB = 32 * PER;
+  uint32_t c[PER], tot = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    c[j] = SHARED ? h[NB - 1 - PER * lane - j] : __ldcg(h + NB - 1 - PER * lane - j);
+    tot += c[j];
+  }
+  uint32_t incl = tot;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  const uint32_t ab0 = incl - tot;
+  const unsigned who = __ballot_sync(0xffffffffu, ab0 < r && r <= incl);
+  const int src = who ? __ffs(who) - 1 : 31;
+  uint32_t dd = 0, ab = ab0;
+  if (lane == src) {
+    dd = (uint32_t)(NB - PER * lane - PER);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (ab + c[j] >= r) {
+        dd = (uint32_t)(NB - 1 - PER * lane - j);
+        break;
+      }
+      ab += c[j];
+    }
+  }
+  d = __shfl_sync(0xffffffffu, dd, src);
+  above = __shfl_sync(0xffffffffu, ab, src);
+}
+
+// Zero `words` (a multiple of 4) 32-bit words of shared memory with 16-B stores.
+__device__ __forceinline__ void zero_words(uint32_t* hw, uint32_t words) {
+  uint4* z = reinterpret_cast<uint4*>(hw);
+  for (uint32_t i = threadIdx.x; i < words / 4u; i += blockDim.x) z[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+// Flush the 64 packed u16 bins of words 32t .. 32t+31 (t = the calling thread's range) into the global
+// fine histogram fine[0 .. 64) (atomics for non-zero bins only; most words are zero), return their total.
+__device__ __forceinline__ uint32_t flush_range(const uint32_t* hw, uint32_t t, unsigned* fine, int lane) {
+  const uint4* h4 = reinterpret_cast<const uint4*>(hw) + 8u * t;
+  uint32_t tot = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int jj = (j + lane) & 7;  // rotated: the 8 threads of a quarter-warp hit distinct banks
+    const uint4 v = h4[jj];
+    if ((v.x | v.y | v.z | v.w) != 0u) {
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t lo16 = wv[c] & 0xffffu, hi16 = wv[c] >> 16;
+        if (lo16) atomicAdd(fine + 8 * jj + 2 * c, lo16);
+        if (hi16) atomicAdd(fine + 8 * jj + 2 * c + 1, hi16);
+        tot += lo16 + hi16;
+      }
+    }
+  }
+  return tot;
+}
+
+// Packed u16 bin counter += 1 for every lane of the warp holding `bin` (warp-aggregated).
+__device__ __forceinline__ void hist_add(uint32_t* hw, bool valid, uint32_t bin, int lane) {
+  const unsigned peers = __match_any_sync(0xffffffffu, valid ? bin : 0xffffffffu);
+  if (valid && (__ffs(peers) - 1) == lane) atomicAdd(hw + (bin >> 1), (uint32_t)__popc(peers) << ((bin & 1u) * 16u));
+}
+
+// (value, multiplicity) of the largest / smallest key seen: merge another pair into (v, c)
+__device__ __forceinline__ void merge_max(uint64_t& v, uint32_t& c, uint64_t v2, uint32_t c2) {
+  c = v2 > v ? c2 : (v2 == v ? c + c2 : c);
+  v = v2 > v ? v2 : v;
+}
+__device__ __forceinline__ void merge_min(uint64_t& v, uint32_t& c, uint64_t v2, uint32_t c2) {
+  c = v2 < v ? c2 : (v2 == v ? c + c2 : c);
+  v = v2 < v ? v2 : v;
+}
+__device__ __forceinline__ void warp_merge_extremes(uint64_t& mx, uint32_t& cx, uint64_t& mn, uint32_t& cn) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, mx, off), b = __shfl_xor_sync(0xffffffffu, mn, off);
+    const uint32_t ca = __shfl_xor_sync(0xffffffffu, cx, off), cb = __shfl_xor_sync(0xffffffffu, cn, off);
+    merge_max(mx, cx, a, ca);
+    merge_min(mn, cn, b, cb);
+  }
+}
+
+// Index of the slot whose key range [slo, shi] holds `key` among `ns` disjoint ranges sorted by slo, else -1.
+__device__ __forceinline__ int find_range(uint64_t key, const uint64_t* slo, const uint64_t* shi, int ns) {
+  if (ns == 0 || key < slo[0]) return -1;
+  int i = 0;
+#pragma unroll
+  for (int step = 8; step > 0; step >>= 1)
+    if (i + step < ns && slo[i + step] <= key) i += step;
+  return key <= shi[i] ? i : -1;
+}
+
+// Warp 0: the distinct key ranges [lo, hi] of the queries q < m with s_mode[q] == mode, sorted ascending
+// (disjoint: equal ranges are one slot), into slo/shi; q2slot[q] = the query's slot; returns the count.
+__device__ __forceinline__ void build_slots(int mode, int m, const int* s_mode, const uint64_t* s_pre,
+                                            const int* s_nbits, uint64_t* slo, uint64_t* shi, int* q2slot, int* nslot,
+                                            int lane) {
+  const bool in = lane < m && s_mode[lane] == mode;
+  uint64_t lo = ~0ull, hi = ~0ull;
+  if (in) {
+    const int rb = 64 - s_nbits[lane];
+    lo = s_pre[lane] << rb;
+    hi = lo | ((1ull << rb) - 1ull);
+  }
+  // distinct ranges: a query leads its range if no lower lane holds the same one
+  bool lead = in;
+  int rank = 0;  // number of distinct ranges below this one
+  for (int j = 0; j < 32; ++j) {
+    const uint64_t lj = __shfl_sync(0xffffffffu, lo, j);
+    const bool inj = __shfl_sync(0xffffffffu, (int)in, j) != 0;
+    if (inj && lj == lo && j < lane) lead = false;
+    // count the leaders below: lane j leads iff no lane < j has its range; evaluated below via ballot
+  }
+  const unsigned leaders = __ballot_sync(0xffffffffu, lead);
+  for (int j = 0; j < 32; ++j) {
+    const uint64_t lj = __shfl_sync(0xffffffffu, lo, j);
+    if (((leaders >> j) & 1u) && lj < lo) ++rank;
+  }
+  if (lead) {
+    slo[rank] = lo;
+    shi[rank] = hi;
+  }
+  if (in) q2slot[lane] = rank;
+  if (lane == 0) *nslot = __popc(leaders);
+}
+
+template <bool CACHED>
+__global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* __restrict__ y, uint64_t n, int m,
+                                                                 SelScratch* __restrict__ S,
+                                                                 const __grid_constant__ SelQueries Q,
+                                                                 double* __restrict__ pml_out, double* __restrict__ tvar_out) {
+  extern __shared__ __align__(16) uint64_t sdyn[];
+  uint64_t* skeys = sdyn;                                        // [kSelCache]
+  uint32_t* hw = reinterpret_cast<uint32_t*>(sdyn + kSelCache);  // [kSelHistWords] packed u16 bins
+  __shared__ uint64_t s_pre[kMaxQ], s_T[kMaxQ], s_up[kMaxQ], s_slo[kMaxQ], s_shi[kMaxQ];
+  __shared__ uint32_t s_r[kMaxQ], s_above[kMaxQ];  // rank inside the bucket; keys above the bucket (or T)
+  __shared__ int s_nbits[kMaxQ], s_mode[kMaxQ], s_q2slot[kMaxQ], s_nslot;
+  __shared__ unsigned long long s_ev[2][32];
+  __shared__ uint32_t s_ec[2][32];
+  __shared__ double wsum[kSelThreads / 32][kMaxQ];
   const unsigned FULL = 0xffffffffu;
   const unsigned nb = gridDim.x;
   const uint64_t lo = n * blockIdx.x / nb, hi = n * (blockIdx.x + 1) / nb;
   const uint32_t cnt = (uint32_t)(hi - lo);
-  const bool cached = (n + nb - 1) / nb <= (uint64_t)kCacheKeys;  // uniform over blocks
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (cached)
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) skeys[i] = to_key(y[lo + i]);
-  if (threadIdx.x < m) {
-    s_prefix[threadIdx.x] = 0;
-    s_rank[threadIdx.x] = Q.k[threadIdx.x];
-    s_q2slot[threadIdx.x] = 0;
+  unsigned bar_target = 0;
+  auto key_at = [&](uint32_t i) -> uint64_t {
+    if constexpr (CACHED) return skeys[i];
+    else return to_key(__ldg(y + lo + i));
+  };
+  int tp = 0;
+  auto stamp = [&]() {  // ARA_METRICS_TRACE: phase boundaries
+    if (threadIdx.x == 0 && tp < 24) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      S->trace[blockIdx.x][tp] = t;
+    }
+    ++tp;
+  };
+  stamp();
+  // ---- zero the pass-H histograms of this launch (this block's share) and the candidate counters
+  {
+    const uint32_t words = (uint32_t)((sizeof(S->HB_c) + sizeof(S->HB_f)) / 4);
+    uint32_t* z = &S->HB_c[0][0][0];
+    const uint32_t per = (words + nb - 1) / nb, b0 = per * blockIdx.x, b1 = min(words, b0 + per);
+    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) z[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x < kMaxQ) S->cand_n[threadIdx.x] = 0u;
   }
-  if (threadIdx.x == 0) {
-    s_nslot = 1;
-    s_slot_prefix[0] = 0;
-    s_nact = cnt;
+  // ---- pass A: cache the keys, histogram the top 16 bits, chunk max/min with multiplicities
+  if constexpr (CACHED) {  // all of a thread's loads in flight at once (<= 8: cnt <= kSelCache)
+    double v[kSelCache / kSelThreads];
+#pragma unroll
+    for (uint32_t j = 0; j < kSelCache / kSelThreads; ++j) {
+      const uint32_t i = threadIdx.x + j * kSelThreads;
+      v[j] = i < cnt ? __ldg(y + lo + i) : 0.0;
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < kSelCache / kSelThreads; ++j) {
+      const uint32_t i = threadIdx.x + j * kSelThreads;
+      if (i < cnt) skeys[i] = to_key(v[j]);
+    }
+  }
+  uint64_t mx = 0, mn = ~0ull;
+  uint32_t cx = 0, cn = 0;
+  for (uint32_t s0 = 0;; s0 += kSelSub) {
+    const uint32_t s1 = min(cnt, s0 + kSelSub);
+    zero_words(hw, kSelHistWords);
+    __syncthreads();
+    stamp();
+    for (uint32_t base = s0; base < s1; base += blockDim.x) {  // warp-uniform trip count
+      const uint32_t i = base + threadIdx.x;
+      const bool valid = i < s1;
+      const uint64_t key = valid ? key_at(i) : 0;
+      if (valid) {
+        merge_max(mx, cx, key, 1u);
+        merge_min(mn, cn, key, 1u);
+      }
+      hist_add(hw, valid, (uint32_t)(key >> 48), lane);
+    }
+    __syncthreads();
+    stamp();
+    {  // thread t: bins 64t .. 64t+63 (a quarter of coarse bin t / 4)
+      uint32_t csum = flush_range(hw, threadIdx.x, S->HA_f + 64u * threadIdx.x, lane);
+      csum += __shfl_xor_sync(FULL, csum, 1);
+      csum += __shfl_xor_sync(FULL, csum, 2);
+      if ((threadIdx.x & 3u) == 0u && csum) atomicAdd(&S->HA_c[threadIdx.x >> 2], csum);
+    }
+    if (s1 >= cnt) break;
+    __syncthreads();
   }
   __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
-  for (int pass = 0; pass < 8; ++pass) {
+  stamp();
+  warp_merge_extremes(mx, cx, mn, cn);
+  if (lane == 0) {
+    s_ev[0][w] = mx;
+    s_ec[0][w] = cx;
+    s_ev[1][w] = mn;
+    s_ec[1][w] = cn;
+  }
+  __syncthreads();
+  if (w == 0) {
+    mx = s_ev[0][lane];
+    cx = s_ec[0][lane];
+    mn = s_ev[1][lane];
+    cn = s_ec[1][lane];
+    warp_merge_extremes(mx, cx, mn, cn);
+    if (lane == 0) {
+      S->bmax[blockIdx.x] = mx;
+      S->bcmax[blockIdx.x] = cx;
+      S->bmin[blockIdx.x] = mn;
+      S->bcmin[blockIdx.x] = cn;
+    }
+  }
+  stamp();
+  grid_sync(&S->bar_count, bar_target += nb);
+  stamp();
+  // ---- after A: warp 31 merges the chunks' extremes; warp 30 stages the coarse histogram in shared memory
+  // (every block reads each global line once: 148 blocks x 13 queries reading the same lines from L2
+  // was a hot spot costing ~10 us); then warp q < m finds query q's 16-bit bucket
+  uint32_t qd = 0, qa = 0, qc = 0;  // warp q: digit, keys above its bucket, bucket size
+  uint32_t* sh_c = hw;              // [256] coarse bins
+  uint32_t* sh_f = hw + 256;        // [m][256] fine bins of each query's coarse digit
+  if (w == 31) {
+    uint64_t gx = 0, gn = ~0ull;
+    uint32_t gcx = 0, gcn = 0;
+    for (uint32_t b = lane; b < nb; b += 32) {
+      merge_max(gx, gcx, __ldcg(&S->bmax[b]), __ldcg(&S->bcmax[b]));
+      merge_min(gn, gcn, __ldcg(&S->bmin[b]), __ldcg(&S->bcmin[b]));
+    }
+    warp_merge_extremes(gx, gcx, gn, gcn);
+    if (lane == 0) {
+      s_ev[0][0] = gx;
+      s_ec[0][0] = gcx;
+      s_ev[1][0] = gn;
+      s_ec[1][0] = gcn;
+    }
+  } else if (w == 30) {
+    const uint4* src = reinterpret_cast<const uint4*>(S->HA_c);
+    reinterpret_cast<uint4*>(sh_c)[lane] = __ldcg(src + lane);
+    reinterpret_cast<uint4*>(sh_c)[lane + 32] = __ldcg(src + lane + 32);
+  }
+  __syncthreads();
+  if (w < m) {
+    const uint32_t k = (uint32_t)Q.k[w];
+    uint32_t dc, ac, df, af;
+    find_digit<8, true>(sh_c, k, lane, dc, ac);
+    uint32_t* f = sh_f + 256u * w;
+    const uint4* src = reinterpret_cast<const uint4*>(S->HA_f + 256u * dc);
+    reinterpret_cast<uint4*>(f)[lane] = __ldcg(src + lane);
+    reinterpret_cast<uint4*>(f)[lane + 32] = __ldcg(src + lane + 32);
+    __syncwarp();
+    find_digit<8, true>(f, k - ac, lane, df, af);
+    qd = 256u * dc + df;
+    qa = ac + af;
+    qc = f[df];
+  }
+  __syncthreads();
+  if (w < m && lane == 0) {  // classify: the rank falls on the global maximum / minimum key, or a bucket
+    const int q = w;
+    const uint32_t k = (uint32_t)Q.k[q], cmx = s_ec[0][0], cmn = s_ec[1][0];
+    if (k <= cmx || k > (uint32_t)n - cmn) {
+      s_mode[q] = kModeDone;
+      s_T[q] = k <= cmx ? s_ev[0][0] : s_ev[1][0];
+      s_above[q] = k <= cmx ? 0u : (uint32_t)n - cmn;
+    } else {
+      s_pre[q] = qd;
+      s_nbits[q] = 16;
+      s_r[q] = k - qa;
+      s_above[q] = qa;
+      s_mode[q] = qc <= kCandCap ? kModeCand : kModeHist;
+    }
+  }
+  __syncthreads();
+  stamp();
+  // ---- passes H: 12 more bits of every bucket still larger than kCandCap
+  for (int hp = 0; hp < kSelHPasses; ++hp) {
+    if (w == 0) build_slots(kModeHist, m, s_mode, s_pre, s_nbits, s_slo, s_shi, s_q2slot, &s_nslot, lane);
+    __syncthreads();
     const int ns = s_nslot;
-    for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) sh[i / 256][i % 256] = 0;
-    if (threadIdx.x == 0) s_nnext = 0;
-    __syncthreads();
-    const int shift = 56 - 8 * pass;
-    const uint32_t nact = cached ? s_nact : cnt;
-    const uint32_t cur_s = act_s + (uint32_t)(pass & 1) * (kCacheKeys * 2u);
-    const uint32_t nxt_s = act_s + (uint32_t)((pass + 1) & 1) * (kCacheKeys * 2u);
-    for (uint32_t base = 0; base < nact; base += blockDim.x) {  // warp-uniform trip count
-      const uint32_t i = base + threadIdx.x;
-      const bool valid = i < nact;
-      uint32_t idx = i;
-      if (pass != 0 && cached && valid) {
-        unsigned short v16;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v16) : "r"(cur_s + 2u * i) : "memory");
-        idx = v16;
+    if (ns == 0) break;  // uniform over the grid: every block derived the same state
+    int nbits = 0;
+    for (int q = 0; q < m; ++q)
+      if (s_mode[q] == kModeHist) nbits = s_nbits[q];  // every HIST query holds the same number of bits
+    const int shift = 52 - nbits;  // digit = bits [shift, shift + 12)
+    const uint64_t rlo = s_slo[0], rhi = s_shi[ns - 1];
+    for (uint32_t s0 = 0;; s0 += kSelSub) {
+      const uint32_t s1 = min(cnt, s0 + kSelSub);
+      zero_words(hw, (uint32_t)ns * 2048u);
+      __syncthreads();
+      for (uint32_t base = s0; base < s1; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const uint64_t key = i < s1 ? key_at(i) : 0;
+        int sl = -1;
+        if (i < s1 && key >= rlo && key <= rhi) sl = find_range(key, s_slo, s_shi, ns);
+        hist_add(hw, sl >= 0, ((uint32_t)sl << 12) | ((uint32_t)(key >> shift) & 0xfffu), lane);
       }
-      const uint64_t key = valid ? (cached ? skeys[idx] : to_key(y[lo + idx])) : 0;
-      const unsigned digit = (unsigned)(key >> shift) & 0xffu;
-      const uint64_t hik = pass == 0 ? 0 : (key >> (shift + 8));
-      // the slots' prefixes are distinct, so a key feeds at most one slot's histogram
-      int sl = -1;
-      if (valid)
-        for (int j = 0; j < ns; ++j)
-          if (hik == s_slot_prefix[j]) sl = j;
-      const unsigned keep = __ballot_sync(FULL, sl >= 0);
-      if (keep == 0u) continue;
-      if (cached) {  // survivors of this pass (order is irrelevant to the histograms)
-        uint32_t at = 0;
-        if (lane == __ffs(keep) - 1) at = atomicAdd(&s_nnext, (uint32_t)__popc(keep));
-        at = __shfl_sync(FULL, at, __ffs(keep) - 1);
-        if (sl >= 0)
-          asm volatile("st.shared.u16 [%0], %1;" ::"r"(nxt_s + 2u * (at + __popc(keep & lt))), "h"((unsigned short)idx)
-                       : "memory");
+      __syncthreads();
+      stamp();
+      if (threadIdx.x < (unsigned)ns * 64u) {  // thread t: slot t / 64, coarse bin t % 64 = words 32t .. 32t+31
+        const uint32_t csum = flush_range(hw, threadIdx.x, &S->HB_f[hp][0][0] + 64u * threadIdx.x, lane);
+        if (csum) atomicAdd(&S->HB_c[hp][threadIdx.x >> 6][threadIdx.x & 63u], csum);
       }
-      const unsigned bin = sl >= 0 ? ((unsigned)sl << 8 | digit) : 0xffffffffu;
-      const unsigned peers = __match_any_sync(FULL, bin);  // warp-aggregated shared atomics
-      if (sl >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&sh[sl][digit], __popc(peers));
+      if (s1 >= cnt) break;
+      __syncthreads();
+    }
+    stamp();
+    grid_sync(&S->bar_count, bar_target += nb);
+    stamp();
+    // stage every slot's 64 coarse bins in shared memory (one read per line per block), then warp q
+    // finds its digit: coarse from shared memory, its 64 fine bins staged per warp
+    {
+      const uint32_t* src = &S->HB_c[hp][0][0];
+      for (uint32_t i = threadIdx.x; i < (uint32_t)ns * 64u; i += blockDim.x) hw[i] = __ldcg(src + i);
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_nact = s_nnext;
-    unsigned int(*H)[256] = st->H[pass % 3];
-    for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) {
-      const unsigned v = sh[i / 256][i % 256];
-      if (v) atomicAdd(&H[i / 256][i % 256], v);
-    }
-    if (blockIdx.x == 0)  // clear the buffer pass+1 will use (last read before the previous barrier)
-      for (int i = threadIdx.x; i < kMaxQ * 256; i += blockDim.x) st->H[(pass + 1) % 3][i / 256][i % 256] = 0;
-    grid_sync(&st->bar_count, &st->bar_gen, nb);
-    for (int i = threadIdx.x; i < ns * 256; i += blockDim.x) sh[i / 256][i % 256] = ((volatile unsigned int*)H[i / 256])[i % 256];
-    __syncthreads();
-    if (w < m) {  // warp q: the digit d of query q's k-th largest key among the keys of its slot
-      const int q = w;
-      const unsigned int* h = sh[s_q2slot[q]];
-      const uint64_t r = s_rank[q];
-      // lane l owns digits 255 - 8l .. 248 - 8l (descending); exclusive prefix of the lane totals
-      uint64_t c[8], tot = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = h[255 - 8 * lane - j];
-        tot += c[j];
-      }
-      uint64_t above = tot;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint64_t o = __shfl_up_sync(FULL, above, off);
-        if (lane >= off) above += o;
-      }
-      above -= tot;  // count of keys in the slot with a larger digit than this lane's bins
-      // the lane whose range holds rank r finds its digit (digit 0 if the rank runs past every bin)
-      const bool mine = above < r && (r <= above + tot || lane == 31);
-      const unsigned who = __ballot_sync(FULL, mine);
-      const int src = __ffs(who) - 1;
-      int d = 0;
-      uint64_t ab = above;
-      if (lane == src) {
-        d = 248 - 8 * lane;  // lowest digit of the range (taken if the rank runs past it)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int dj = 255 - 8 * lane - j;
-          if (ab + c[j] >= r) {
-            d = dj;
-            break;
-          }
-          if (dj == 0) {  // rank beyond the slot's keys cannot happen for a valid k; keep digit 0
-            d = 0;
-            break;
-          }
-          ab += c[j];
+    if (w < m && s_mode[w] == kModeHist) {
+      const int q = w, sl = s_q2slot[q];
+      uint32_t dc, ac, df, af;
+      const uint32_t r = s_r[q];
+      find_digit<2, true>(hw + 64u * sl, r, lane, dc, ac);
+      uint32_t* f = hw + 1024u + 64u * w;
+      const uint32_t* fsrc = S->HB_f[hp][sl] + 64u * dc;
+      f[lane] = __ldcg(fsrc + lane);
+      f[lane + 32] = __ldcg(fsrc + lane + 32);
+      __syncwarp();
+      find_digit<2, true>(f, r - ac, lane, df, af);
+      const uint32_t d = 64u * dc + df;
+      if (lane == 0) {
+        const uint32_t c = f[df];
+        const uint64_t pre = (s_pre[q] << 12) | d;
+        s_pre[q] = pre;
+        s_nbits[q] = nbits + 12;
+        s_r[q] = r - ac - af;
+        s_above[q] += ac + af;
+        if (nbits + 12 == 64) {
+          s_mode[q] = kModeDone;
+          s_T[q] = pre;
+        } else {
+          s_mode[q] = c <= kCandCap ? kModeCand : kModeHist;
         }
       }
-      d = __shfl_sync(FULL, d, src);
-      ab = __shfl_sync(FULL, ab, src);
-      if (lane == 0) {
-        s_rank[q] = r - ab;
-        s_prefix[q] = (s_prefix[q] << 8) | (uint64_t)d;
-      }
     }
     __syncthreads();
-    if (w == 0) {  // slots = distinct prefixes, numbered in query order
-      const uint64_t pq = lane < m ? s_prefix[lane] : ~0ull;
-      int first = lane;
-      for (int q2 = 0; q2 < m; ++q2)
-        if (q2 < first && s_prefix[q2] == pq) first = q2;
-      const unsigned leaders = __ballot_sync(FULL, lane < m && first == lane);
-      if (lane < m) {
-        const int sl = __popc(leaders & ((1u << first) - 1u));
-        s_q2slot[lane] = sl;
-        if (first == lane) s_slot_prefix[sl] = pq;
-      }
-      if (lane == 0) s_nslot = __popc(leaders);
-    }
-    __syncthreads();
+    stamp();
   }
-  // tail: count and fp64-sum the values above each query's threshold T (fixed reduction order), four
-  // queries per sweep over the keys (each key decoded once per sweep; every query still adds its keys
-  // in the same thread order as a query-at-a-time loop)
-  for (int q0 = 0; q0 < m; q0 += 4) {
-    uint64_t pq[4];
-    double a[4] = {0.0, 0.0, 0.0, 0.0};
-    uint32_t b[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) pq[j] = q0 + j < m ? s_prefix[q0 + j] : ~0ull;  // no key exceeds ~0
+  stamp();
+  // ---- pass C: compact the candidate buckets; per query, sum the values above its bucket (or above T)
+  if (w == 0) build_slots(kModeCand, m, s_mode, s_pre, s_nbits, s_slo, s_shi, s_q2slot, &s_nslot, lane);
+  if (threadIdx.x >= 32 && threadIdx.x < 32u + (unsigned)m) {  // per query: the largest key it does not sum
+    const int q = threadIdx.x - 32;
+    const int rb = 64 - s_nbits[q];
+    s_up[q] = s_mode[q] == kModeDone ? s_T[q] : ((s_pre[q] << rb) | ((1ull << rb) - 1ull));
+  }
+  __syncthreads();
+  const int nc = s_nslot;
+  if (nc > 0) {  // block-local lists in shared memory, then one global reservation per slot
+    uint64_t* lc = reinterpret_cast<uint64_t*>(hw);  // [nc][kCandCap]
+    __shared__ uint32_t s_ln[kMaxQ], s_lbase[kMaxQ];
+    if (threadIdx.x < (unsigned)nc) s_ln[threadIdx.x] = 0u;
+    __syncthreads();
+    const uint64_t rlo = s_slo[0], rhi = s_shi[nc - 1];
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-      const uint64_t key = cached ? skeys[i] : to_key(y[lo + i]);
+      const uint64_t key = key_at(i);
+      if (key >= rlo && key <= rhi) {
+        const int sl = find_range(key, s_slo, s_shi, nc);
+        if (sl >= 0) lc[sl * kCandCap + atomicAdd(&s_ln[sl], 1u)] = key;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < (unsigned)nc && s_ln[threadIdx.x])
+      s_lbase[threadIdx.x] = atomicAdd(&S->cand_n[threadIdx.x], s_ln[threadIdx.x]);
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < (uint32_t)nc * kCandCap; e += blockDim.x) {
+      const uint32_t sl = e / kCandCap, i = e % kCandCap;
+      if (i < s_ln[sl]) S->cand[sl][s_lbase[sl] + i] = lc[e];
+    }
+  }
+  stamp();
+  // fp64 sums of the values above s_up, eight queries per sweep (fixed thread order; counts are known)
+  for (int q0 = 0; q0 < m; q0 += 8) {
+    uint64_t up[8];
+    double a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      up[j] = q0 + j < m ? s_up[q0 + j] : ~0ull;  // no key exceeds ~0
+      a[j] = 0.0;
+    }
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const uint64_t key = key_at(i);
       const double v = from_key(key);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (key > pq[j]) {
-          a[j] += v;
-          b[j] += 1u;
-        }
+      for (int j = 0; j < 8; ++j)
+        if (key > up[j]) a[j] += v;
     }
+    stamp();
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      double aj = a[j];
-      unsigned long long bj = b[j];
-      for (int off = 16; off > 0; off >>= 1) {
-        aj += __shfl_xor_sync(FULL, aj, off);
-        bj += __shfl_xor_sync(FULL, bj, off);
-      }
-      if (lane == 0 && q0 + j < m) {
-        wsum[w][q0 + j] = aj;
-        wcnt[w][q0 + j] = bj;
+    for (int j = 0; j < 8; ++j) {
+      if (q0 + j < m) {  // warp-uniform
+        double aj = a[j];
+        for (int off = 16; off > 0; off >>= 1) aj += __shfl_xor_sync(FULL, aj, off);
+        if (lane == 0) wsum[w][q0 + j] = aj;
       }
     }
   }
   __syncthreads();
-  if (threadIdx.x < m) {
+  if (threadIdx.x < (unsigned)m) {
     double a = 0.0;
-    unsigned long long b = 0;
-    for (int i = 0; i < kFusedBlock / 32; ++i) {
-      a += wsum[i][threadIdx.x];
-      b += wcnt[i][threadIdx.x];
-    }
-    psum[(uint64_t)blockIdx.x * kMaxQ + threadIdx.x] = a;
-    pcnt[(uint64_t)blockIdx.x * kMaxQ + threadIdx.x] = b;
+    for (int i = 0; i < kSelThreads / 32; ++i) a += wsum[i][threadIdx.x];
+    S->psum[blockIdx.x][threadIdx.x] = a;
   }
-  grid_sync(&st->bar_count, &st->bar_gen, nb);
+  stamp();
+  grid_sync(&S->bar_count, bar_target += nb);
+  stamp();
+  if (threadIdx.x == 0 && atomicAdd(&S->bar_exit, 1u) == nb - 1) {  // every block is past the last barrier
+    S->bar_count = 0u;
+    S->bar_exit = 0u;
+  }
+  {  // pass A's histogram has had its last reader: zero it for the next launch (this block's share)
+    const uint32_t words = 256u + 65536u;
+    uint32_t* z = S->HA_c;
+    const uint32_t per = (words + nb - 1) / nb, b0 = per * blockIdx.x, b1 = min(words, b0 + per);
+    for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) z[i] = 0u;
+  }
   if (blockIdx.x != 0) return;
-  if (w < m) {  // warp q combines the block partials of query q in a fixed order
+  // ---- F (block 0): sort each candidate list descending (position = keys above + equal keys listed
+  // before: distinct positions, and equal keys are equal values), then per query T and TVaR
+  uint64_t* craw = reinterpret_cast<uint64_t*>(hw);  // [nc][kCandCap] as compacted (any order)
+  uint64_t* cs = craw + kMaxQ * kCandCap;              // [nc][kCandCap] sorted descending
+  __shared__ uint32_t s_cn[kMaxQ];
+  if (threadIdx.x < (unsigned)nc) s_cn[threadIdx.x] = __ldcg(&S->cand_n[threadIdx.x]);
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e < (uint32_t)nc * kCandCap; e += blockDim.x)
+    if (e % kCandCap < s_cn[e / kCandCap]) craw[e] = __ldcg(&S->cand[0][0] + e);
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e < (uint32_t)nc * kCandCap; e += blockDim.x) {
+    const uint32_t sl = e / kCandCap, i = e % kCandCap, nn = s_cn[sl];
+    if (i >= nn) continue;
+    const uint64_t* c = craw + sl * kCandCap;
+    const uint64_t ki = c[i];
+    uint32_t pos = 0;
+    for (uint32_t j = 0; j < nn; ++j) pos += (c[j] > ki) || (c[j] == ki && j < i);
+    cs[sl * kCandCap + pos] = ki;
+  }
+  __syncthreads();
+  if (w < m) {
     const int q = w;
     double a = 0.0;
-    unsigned long long b = 0;
-    for (unsigned i = lane; i < nb; i += 32) {
-      a += ((volatile double*)psum)[(uint64_t)i * kMaxQ + q];
-      b += ((volatile unsigned long long*)pcnt)[(uint64_t)i * kMaxQ + q];
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-      a += __shfl_xor_sync(FULL, a, off);
-      b += __shfl_xor_sync(FULL, b, off);
-    }
+    for (unsigned i = lane; i < nb; i += 32) a += __ldcg(&S->psum[i][q]);
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
     if (lane == 0) {
-      const double T = from_key(s_prefix[q]);
+      uint64_t T, b = s_above[q];
+      if (s_mode[q] == kModeDone) {
+        T = s_T[q];
+      } else {  // the candidates of the bucket, descending: T is the rank's key; add those above T in order
+        const uint64_t* c = cs + s_q2slot[q] * kCandCap;
+        const uint32_t r = s_r[q];
+        T = c[r - 1];
+        for (uint32_t j = 0; j < r - 1 && c[j] > T; ++j) {
+          a += from_key(c[j]);
+          b += 1;
+        }
+      }
+      const double Tv = from_key(T);
       const uint64_t k = Q.k[q];
-      if (pml_out) pml_out[q] = T;  // PML: the k-th largest value
-      if (tvar_out) tvar_out[q] = __ddiv_rn(__dadd_rn(a, __dmul_rn((double)(k - b), T)), (double)k);  // TVaR
+      if (pml_out) pml_out[q] = Tv;  // PML: the k-th largest value
+      if (tvar_out) tvar_out[q] = __ddiv_rn(__dadd_rn(a, __dmul_rn((double)(k - b), Tv)), (double)k);  // TVaR
     }
   }
+  __syncthreads();
+  stamp();
 }
 
-// Per-device launch facts of the fused kernel, queried once (host-side cache; no per-call queries).
+// Per-device launch facts of metrics_select, queried once (host-side cache; no per-call queries).
 struct FusedInfo {
   int ready = 0, coop = 0, sms = 148, occ = 0;
 };
 static FusedInfo g_fused[64];
+constexpr size_t kSelDynSmem = (size_t)kSelCache * sizeof(uint64_t) + (size_t)kSelHistWords * sizeof(uint32_t);
 
 static const FusedInfo& fused_info() {
   int dev = 0;
@@ -500,44 +815,47 @@ static const FusedInfo& fused_info() {
     cudaGetLastError();
     cudaDeviceGetAttribute(&f.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&f.coop, cudaDevAttrCooperativeLaunch, dev);
-    const size_t dyn = (size_t)kCacheKeys * (sizeof(uint64_t) + 2 * sizeof(uint16_t));
-    cudaFuncSetAttribute((const void*)metrics_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f.occ, (const void*)metrics_fused, kFusedBlock, dyn) != cudaSuccess) {
+    int occ_u = 0;
+    cudaFuncSetAttribute((const void*)metrics_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelDynSmem);
+    cudaFuncSetAttribute((const void*)metrics_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelDynSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f.occ, (const void*)metrics_select<true>, kSelThreads, kSelDynSmem) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_u, (const void*)metrics_select<false>, kSelThreads, kSelDynSmem) !=
+            cudaSuccess) {
       cudaGetLastError();
       f.occ = 0;
     }
+    f.occ = std::min(f.occ, occ_u);
     f.ready = 1;
   }
   return f;
 }
 
-// Launch the fused kernel cooperatively for one batch of <= kMaxQ queries, results to DEVICE pml/tvar
-// (either may be null); asynchronous.  Returns false if the device refuses a cooperative launch of the
-// needed size (callers fall back to the pass kernels).
+// Launch metrics_select cooperatively for one batch of <= kMaxQ queries, results to DEVICE pml/tvar
+// (either may be null); asynchronous.  `zeroed`: the scratch is known to hold zeros where the kernel
+// expects them (a plan's scratch after its first use); otherwise it is cleared first.  Returns false if
+// the device refuses a cooperative launch of the needed size (callers fall back to the pass kernels).
 static bool metrics_fused_batch(const double* ylt, uint64_t n, int mq, const uint64_t* ks, char* scratch,
                                 size_t scratch_bytes, double* pml_dev, double* tvar_dev, cudaStream_t s,
-                                cudaError_t* err) {
+                                cudaError_t* err, bool zeroed = false) {
   *err = cudaSuccess;
   const FusedInfo& f = fused_info();
-  if (!f.coop || f.occ < 1) return false;
-  const size_t dyn = (size_t)kCacheKeys * (sizeof(uint64_t) + 2 * sizeof(uint16_t));
+  if (!f.coop || f.occ < 1 || n > 0xffffffffull) return false;
   uint64_t grid = (uint64_t)f.sms * f.occ;
-  const uint64_t need = (n + kFusedBlock - 1) / kFusedBlock;
+  const uint64_t need = (n + kSelThreads - 1) / kSelThreads;
   if (grid > need) grid = need;
-  const size_t state = sizeof(FusedState);
-  const size_t need_bytes = state + grid * kMaxQ * (sizeof(double) + sizeof(unsigned long long));
-  if (need_bytes > scratch_bytes) return false;
-  FusedState* st = (FusedState*)scratch;
-  double* psum = (double*)(scratch + state);
-  unsigned long long* pcnt = (unsigned long long*)(psum + grid * kMaxQ);
-  FusedQueries Q;
+  if (grid > (uint64_t)kSelMaxBlocks) grid = kSelMaxBlocks;
+  if (sizeof(SelScratch) > scratch_bytes) return false;
+  SelScratch* st = (SelScratch*)scratch;
+  SelQueries Q;
   memset(&Q, 0, sizeof Q);
   for (int q = 0; q < mq; ++q) Q.k[q] = ks[q];
-  if ((*err = cudaMemsetAsync(st, 0, sizeof(FusedState), s)) != cudaSuccess) return true;
+  if (!zeroed && (*err = cudaMemsetAsync(st, 0, sizeof(SelScratch), s)) != cudaSuccess) return true;
   int m_ = mq;
-  void* args[] = {(void*)&ylt, (void*)&n, (void*)&m_, (void*)&st, (void*)&psum, (void*)&pcnt, (void*)&Q,
-                  (void*)&pml_dev, (void*)&tvar_dev};
-  *err = cudaLaunchCooperativeKernel((const void*)metrics_fused, dim3((unsigned)grid), dim3(kFusedBlock), args, dyn, s);
+  void* args[] = {(void*)&ylt, (void*)&n, (void*)&m_, (void*)&st, (void*)&Q, (void*)&pml_dev, (void*)&tvar_dev};
+  const bool cached = (n + grid - 1) / grid <= (uint64_t)kSelCache;  // every block's chunk fits its key cache
+  *err = cudaLaunchCooperativeKernel(cached ? (const void*)metrics_select<true> : (const void*)metrics_select<false>,
+                                     dim3((unsigned)grid), dim3(kSelThreads), args, kSelDynSmem, s);
   return true;
 }
 
@@ -562,16 +880,19 @@ static ara_status ranks_for(uint64_t n, const double* rps, uint32_t m, std::vect
   return ARA_OK;
 }
 
-// Scratch: [2*kMaxQ doubles of batch results][state][block partials].
-static size_t scratch_bytes(uint64_t n, uint64_t* blocks_out) {
+// Scratch: [2*kMaxQ doubles of batch results][the pass kernels' state + block partials, or metrics_select's
+// SelScratch, whichever is larger].
+static size_t pass_scratch_bytes(uint64_t n, uint64_t* blocks_out) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   uint64_t blocks = (n + kSelBlock - 1) / kSelBlock;
-  if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;  // covers the fused grid (<= SMs x occupancy)
+  if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
   *blocks_out = blocks;
-  return 2 * kMaxQ * sizeof(double) + std::max(sizeof(SelState), sizeof(FusedState)) +
-         blocks * kMaxQ * (sizeof(double) + sizeof(unsigned long long));
+  return sizeof(SelState) + blocks * kMaxQ * (sizeof(double) + sizeof(unsigned long long));
+}
+static size_t scratch_bytes(uint64_t n, uint64_t* blocks_out) {
+  return 2 * kMaxQ * sizeof(double) + std::max(pass_scratch_bytes(n, blocks_out), sizeof(SelScratch));
 }
 
 static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml, double* tvar,
@@ -590,7 +911,7 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
   char* rest = scratch + 2 * kMaxQ * sizeof(double);
   const size_t rest_bytes = bytes - 2 * kMaxQ * sizeof(double);
   SelState* st = (SelState*)rest;
-  double* psum = (double*)(rest + std::max(sizeof(SelState), sizeof(FusedState)));
+  double* psum = (double*)(rest + sizeof(SelState));
   unsigned long long* pcnt = (unsigned long long*)(psum + blocks * kMaxQ);
   std::vector<double> h_out(2 * kMaxQ);
   SelState init;
@@ -616,6 +937,27 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
         e = cudaGetLastError();
       }
     }
+    if (e == cudaSuccess && use_fused && getenv("ARA_METRICS_TRACE")) {  // development aid: phase times
+      std::vector<unsigned long long> tr((size_t)kSelMaxBlocks * 24);
+      const int nbk = (int)std::min<uint64_t>((n + kSelThreads - 1) / kSelThreads, (uint64_t)fused_info().sms);
+      if (cudaMemcpyAsync(tr.data(), ((SelScratch*)rest)->trace, tr.size() * 8, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+          cudaStreamSynchronize(s) == cudaSuccess) {
+        unsigned long long t0 = ~0ull;
+        for (int b = 0; b < nbk; ++b) t0 = std::min(t0, tr[(size_t)b * 24]);
+        fprintf(stderr, "metrics_select stamps (us from first block start: min/max over %d blocks):", nbk);
+        for (int i = 0; i < 24; ++i) {
+          unsigned long long a = ~0ull, z = 0;
+          for (int b = 0; b < nbk; ++b) {
+            const unsigned long long t = tr[(size_t)b * 24 + i];
+            a = std::min(a, t);
+            z = std::max(z, t);
+          }
+          if (a < t0 || z - t0 > 100000000ull) break;
+          fprintf(stderr, " [%d] %.1f/%.1f", i, (a - t0) * 1e-3, (z - t0) * 1e-3);
+        }
+        fprintf(stderr, "\n");
+      }
+    }
     if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.data(), d_out, 2 * kMaxQ * sizeof(double), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
@@ -633,9 +975,10 @@ static ara_status metrics(const double* ylt, uint64_t n, const double* rps, uint
 
 // Asynchronous variant into caller-provided device scratch (metrics_scratch_size(n) bytes): results to
 // DEVICE pml_dev[m] / tvar_dev[m]; needs cooperative launch.  No allocation, no synchronisation, so it
-// can be captured into a CUDA graph (ara_plan_create).
+// can be captured into a CUDA graph (ara_plan_create).  `zeroed`: the scratch was zeroed when allocated
+// and only ever used by these launches (they leave it as they found it), so no clearing memset is needed.
 ara_status metrics_device_into(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
-                               double* tvar_dev, char* scratch, size_t bytes, cudaStream_t s) {
+                               double* tvar_dev, char* scratch, size_t bytes, cudaStream_t s, bool zeroed) {
   if (!ylt || (!pml_dev && !tvar_dev)) return set_error(ARA_E_ARG, "NULL argument");
   std::vector<uint64_t> ks;
   ara_status rc = ranks_for(n, rps, m, ks);
@@ -644,7 +987,7 @@ ara_status metrics_device_into(const double* ylt, uint64_t n, const double* rps,
     const int mq = (int)std::min<uint32_t>(kMaxQ, m - q0);
     cudaError_t e = cudaSuccess;
     if (!metrics_fused_batch(ylt, n, mq, &ks[q0], scratch, bytes, pml_dev ? pml_dev + q0 : nullptr,
-                             tvar_dev ? tvar_dev + q0 : nullptr, s, &e))
+                             tvar_dev ? tvar_dev + q0 : nullptr, s, &e, zeroed))
       rc = set_error(ARA_E_UNSUPPORTED, "cooperative launch unavailable for the asynchronous metrics");
     else if (e != cudaSuccess)
       rc = cuda_error(e, "fused metric kernel");
@@ -664,7 +1007,7 @@ static ara_status metrics_device(const double* ylt, uint64_t n, const double* rp
   const size_t bytes = metrics_scratch_size(n);
   char* scratch = nullptr;
   ARA_CUDA(cudaMallocAsync((void**)&scratch, bytes, s));
-  ara_status rc = metrics_device_into(ylt, n, rps, m, pml_dev, tvar_dev, scratch, bytes, s);
+  ara_status rc = metrics_device_into(ylt, n, rps, m, pml_dev, tvar_dev, scratch, bytes, s, false);
   cudaFreeAsync(scratch, s);
   return rc;
 }

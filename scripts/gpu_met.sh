@@ -1,0 +1,8 @@
+#!/bin/bash
+TAG=${1:-met}
+O=gpurun_out; mkdir -p $O
+timeout 600 python -m pytest tests -m gpu -q -k "metric or fullsize or plan or dist" > $O/pytest_met_$TAG.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_met_$TAG.log
+timeout 600 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-cold > $O/bench_P_$TAG.json 2> $O/bench_P_$TAG.err; echo "bench rc=$?"
+python -c "
+import json;d=json.loads(open('$O/bench_P_$TAG.json').read().strip().splitlines()[-1]);print('step',d['ms_per_step'],'kernel',d['kernel_ms_per_step'],'metrics',d['gather_metrics_ms_per_step'])"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:metrics_select -s 2 -c 1 -o $O/prof_met_$TAG -f python bench.py --steps 2 --warmup 1 --profile > $O/ncu_met_$TAG.log 2>&1; echo "ncu rc=$?"
