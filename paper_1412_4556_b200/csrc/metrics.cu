@@ -11,6 +11,7 @@
 // are bitwise reproducible run to run.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stddef.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -252,25 +253,30 @@ __global__ void __launch_bounds__(kSelBlock) tail_pass(const double* __restrict_
 constexpr int kSelThreads = 1024;
 constexpr uint32_t kSelCache = 8192;      // cached keys per block (64 KB): n <= 8192 * SMs is read once
 constexpr uint32_t kSelHistWords = 32768; // 128 KB of packed u16 bin counters
+constexpr uint32_t kSelMapWords = 2048 + 512;  // 16-bit slot map: 65,536-bit presence + 2,048 u8 word bases
 constexpr uint32_t kSelSub = 65535;       // keys per histogram sub-chunk (a u16 counter cannot overflow)
 constexpr uint32_t kCandCap = 256;        // bucket size compacted instead of narrowed further
-constexpr int kSelMaxBlocks = 256;
+constexpr int kSelMaxBlocks = 160;      // >= the SM count (148 on B200): one block per SM
 constexpr int kSelHPasses = 4;            // 16 + 4 x 12 = 64 bits
 enum : int { kModeHist = 0, kModeCand = 1, kModeDone = 2 };
 
-struct alignas(16) SelScratch {  // global scratch of metrics_select (zeroed once at allocation)
+struct alignas(16) SelScratch {  // global scratch of metrics_select
+  // -- must hold zeros when a launch starts (cleared when the scratch is allocated; every launch leaves
+  //    them zero again)
   unsigned bar_count, bar_exit;
-  unsigned long long trace[kSelMaxBlocks][24];  // ARA_METRICS_TRACE: every block's %globaltimer at phase boundaries
-  unsigned cand_n[kMaxQ];
-  unsigned long long bmax[kSelMaxBlocks], bmin[kSelMaxBlocks];
-  unsigned bcmax[kSelMaxBlocks], bcmin[kSelMaxBlocks];
-  unsigned long long cand[kMaxQ][kCandCap];
-  double psum[kSelMaxBlocks][kMaxQ];
   alignas(16) unsigned HA_c[256];
   alignas(16) unsigned HA_f[65536];
+  // -- written before they are read within a launch
   alignas(16) unsigned HB_c[kSelHPasses][kMaxQ][64];
   alignas(16) unsigned HB_f[kSelHPasses][kMaxQ][4096];
+  unsigned long long bmax[kSelMaxBlocks], bmin[kSelMaxBlocks];
+  unsigned bcmax[kSelMaxBlocks], bcmin[kSelMaxBlocks];
+  unsigned cand_bn[kMaxQ][kSelMaxBlocks];                     // candidates of slot s held by block b
+  double psum[kSelMaxBlocks][kMaxQ];
+  unsigned long long trace[kSelMaxBlocks][24];                // ARA_METRICS_TRACE: %globaltimer per block and phase
+  unsigned long long cand_b[kSelMaxBlocks][kMaxQ][kCandCap];  // block b's candidates of slot s
 };
+constexpr size_t kSelZeroBytes = offsetof(SelScratch, HB_c);  // the part a fresh scratch must have zeroed
 
 struct SelQueries {  // kernel parameter
   uint64_t k[kMaxQ];
@@ -360,8 +366,7 @@ __device__ __forceinline__ uint32_t flush_range(const uint32_t* hw, uint32_t t, 
 
 // Packed u16 bin counter += 1 for every lane of the warp holding `bin` (warp-aggregated).
 __device__ __forceinline__ void hist_add(uint32_t* hw, bool valid, uint32_t bin, int lane) {
-  const unsigned peers = __match_any_sync(0xffffffffu, valid ? bin : 0xffffffffu);
-  if (valid && (__ffs(peers) - 1) == lane) atomicAdd(hw + (bin >> 1), (uint32_t)__popc(peers) << ((bin & 1u) * 16u));
+  if (valid) atomicAdd(hw + (bin >> 1), 1u << ((bin & 1u) * 16u));
 }
 
 // (value, multiplicity) of the largest / smallest key seen: merge another pair into (v, c)
@@ -408,14 +413,13 @@ __device__ __forceinline__ void build_slots(int mode, int m, const int* s_mode, 
   // distinct ranges: a query leads its range if no lower lane holds the same one
   bool lead = in;
   int rank = 0;  // number of distinct ranges below this one
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < m; ++j) {
     const uint64_t lj = __shfl_sync(0xffffffffu, lo, j);
     const bool inj = __shfl_sync(0xffffffffu, (int)in, j) != 0;
     if (inj && lj == lo && j < lane) lead = false;
-    // count the leaders below: lane j leads iff no lane < j has its range; evaluated below via ballot
   }
   const unsigned leaders = __ballot_sync(0xffffffffu, lead);
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < m; ++j) {
     const uint64_t lj = __shfl_sync(0xffffffffu, lo, j);
     if (((leaders >> j) & 1u) && lj < lo) ++rank;
   }
@@ -431,10 +435,12 @@ template <bool CACHED>
 __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* __restrict__ y, uint64_t n, int m,
                                                                  SelScratch* __restrict__ S,
                                                                  const __grid_constant__ SelQueries Q,
-                                                                 double* __restrict__ pml_out, double* __restrict__ tvar_out) {
+                                                                 double* __restrict__ pml_out, double* __restrict__ tvar_out,
+                                                                 int trace) {
   extern __shared__ __align__(16) uint64_t sdyn[];
   uint64_t* skeys = sdyn;                                        // [kSelCache]
   uint32_t* hw = reinterpret_cast<uint32_t*>(sdyn + kSelCache);  // [kSelHistWords] packed u16 bins
+  uint32_t* smap = hw + kSelHistWords;  // first H pass: bit d = 16-bit prefix d is a slot; then u8 bases
   __shared__ uint64_t s_pre[kMaxQ], s_T[kMaxQ], s_up[kMaxQ], s_slo[kMaxQ], s_shi[kMaxQ];
   __shared__ uint32_t s_r[kMaxQ], s_above[kMaxQ];  // rank inside the bucket; keys above the bucket (or T)
   __shared__ int s_nbits[kMaxQ], s_mode[kMaxQ], s_q2slot[kMaxQ], s_nslot;
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
   };
   int tp = 0;
   auto stamp = [&]() {  // ARA_METRICS_TRACE: phase boundaries
-    if (threadIdx.x == 0 && tp < 24) {
+    if (trace && threadIdx.x == 0 && tp < 24) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       S->trace[blockIdx.x][tp] = t;
@@ -467,7 +473,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
     uint32_t* z = &S->HB_c[0][0][0];
     const uint32_t per = (words + nb - 1) / nb, b0 = per * blockIdx.x, b1 = min(words, b0 + per);
     for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) z[i] = 0u;
-    if (blockIdx.x == 0 && threadIdx.x < kMaxQ) S->cand_n[threadIdx.x] = 0u;
   }
   // ---- pass A: cache the keys, histogram the top 16 bits, chunk max/min with multiplicities
   if constexpr (CACHED) {  // all of a thread's loads in flight at once (<= 8: cnt <= kSelCache)
@@ -606,6 +611,22 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
       if (s_mode[q] == kModeHist) nbits = s_nbits[q];  // every HIST query holds the same number of bits
     const int shift = 52 - nbits;  // digit = bits [shift, shift + 12)
     const uint64_t rlo = s_slo[0], rhi = s_shi[ns - 1];
+    // 16-bit buckets (the first H pass): slot of a key = rank of its 16-bit prefix among the slots' prefixes,
+    // from a 65,536-bit map and per-word bases (no search); deeper prefixes use find_range
+    const bool map16 = nbits == 16;
+    uint8_t* mbase = reinterpret_cast<uint8_t*>(smap + 2048);
+    if (map16) {
+      for (uint32_t i = threadIdx.x; i < 2048u; i += blockDim.x) {
+        uint32_t bits = 0, below = 0;
+        for (int j = 0; j < ns; ++j) {
+          const uint32_t d = (uint32_t)(s_slo[j] >> 48);
+          bits |= (d >> 5) == i ? 1u << (d & 31u) : 0u;
+          below += (d >> 5) < i ? 1u : 0u;
+        }
+        smap[i] = bits;
+        mbase[i] = (uint8_t)below;
+      }
+    }
     for (uint32_t s0 = 0;; s0 += kSelSub) {
       const uint32_t s1 = min(cnt, s0 + kSelSub);
       zero_words(hw, (uint32_t)ns * 2048u);
@@ -614,7 +635,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
         const uint32_t i = base + threadIdx.x;
         const uint64_t key = i < s1 ? key_at(i) : 0;
         int sl = -1;
-        if (i < s1 && key >= rlo && key <= rhi) sl = find_range(key, s_slo, s_shi, ns);
+        if (i < s1 && key >= rlo && key <= rhi) {
+          if (map16) {
+            const uint32_t d = (uint32_t)(key >> 48), bits = smap[d >> 5], b = 1u << (d & 31u);
+            if (bits & b) sl = (int)mbase[d >> 5] + __popc(bits & (b - 1u));
+          } else {
+            sl = find_range(key, s_slo, s_shi, ns);
+          }
+        }
         hist_add(hw, sl >= 0, ((uint32_t)sl << 12) | ((uint32_t)(key >> shift) & 0xfffu), lane);
       }
       __syncthreads();
@@ -676,9 +704,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
   }
   __syncthreads();
   const int nc = s_nslot;
-  if (nc > 0) {  // block-local lists in shared memory, then one global reservation per slot
+  if (nc > 0) {  // block-local lists in shared memory, then copied to this block's region (no global atomics)
     uint64_t* lc = reinterpret_cast<uint64_t*>(hw);  // [nc][kCandCap]
-    __shared__ uint32_t s_ln[kMaxQ], s_lbase[kMaxQ];
+    __shared__ uint32_t s_ln[kMaxQ];
     if (threadIdx.x < (unsigned)nc) s_ln[threadIdx.x] = 0u;
     __syncthreads();
     const uint64_t rlo = s_slo[0], rhi = s_shi[nc - 1];
@@ -690,12 +718,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
       }
     }
     __syncthreads();
-    if (threadIdx.x < (unsigned)nc && s_ln[threadIdx.x])
-      s_lbase[threadIdx.x] = atomicAdd(&S->cand_n[threadIdx.x], s_ln[threadIdx.x]);
-    __syncthreads();
+    if (threadIdx.x < (unsigned)nc) S->cand_bn[threadIdx.x][blockIdx.x] = s_ln[threadIdx.x];
     for (uint32_t e = threadIdx.x; e < (uint32_t)nc * kCandCap; e += blockDim.x) {
       const uint32_t sl = e / kCandCap, i = e % kCandCap;
-      if (i < s_ln[sl]) S->cand[sl][s_lbase[sl] + i] = lc[e];
+      if (i < s_ln[sl]) S->cand_b[blockIdx.x][sl][i] = lc[e];
     }
   }
   stamp();
@@ -750,10 +776,32 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
   uint64_t* craw = reinterpret_cast<uint64_t*>(hw);  // [nc][kCandCap] as compacted (any order)
   uint64_t* cs = craw + kMaxQ * kCandCap;              // [nc][kCandCap] sorted descending
   __shared__ uint32_t s_cn[kMaxQ];
-  if (threadIdx.x < (unsigned)nc) s_cn[threadIdx.x] = __ldcg(&S->cand_n[threadIdx.x]);
+  uint32_t* boff = reinterpret_cast<uint32_t*>(cs + kMaxQ * kCandCap);  // [nc][nb] offsets of the blocks' lists
+  uint32_t* bcnt = boff + kMaxQ * kSelMaxBlocks;                          // [nc][nb] their lengths
+  if (w < nc) {  // warp s: the blocks' counts of slot s, exclusive prefix in block order
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < nb; b0 += 32) {
+      const uint32_t b = b0 + lane;
+      const uint32_t c = b < nb ? __ldcg(&S->cand_bn[w][b]) : 0u;
+      uint32_t incl = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(FULL, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (b < nb) {
+        boff[w * nb + b] = carry + incl - c;
+        bcnt[w * nb + b] = c;
+      }
+      carry += __shfl_sync(FULL, incl, 31);
+    }
+    if (lane == 0) s_cn[w] = carry;
+  }
   __syncthreads();
-  for (uint32_t e = threadIdx.x; e < (uint32_t)nc * kCandCap; e += blockDim.x)
-    if (e % kCandCap < s_cn[e / kCandCap]) craw[e] = __ldcg(&S->cand[0][0] + e);
+  for (uint32_t e = threadIdx.x; e < (uint32_t)nc * nb; e += blockDim.x) {  // (slot, block): copy its list
+    const uint32_t sl = e / nb, b = e % nb, o = boff[e], c = bcnt[e];
+    for (uint32_t i = 0; i < c; ++i) craw[sl * kCandCap + o + i] = __ldcg(&S->cand_b[b][sl][i]);
+  }
   __syncthreads();
   for (uint32_t e = threadIdx.x; e < (uint32_t)nc * kCandCap; e += blockDim.x) {
     const uint32_t sl = e / kCandCap, i = e % kCandCap, nn = s_cn[sl];
@@ -798,7 +846,8 @@ struct FusedInfo {
   int ready = 0, coop = 0, sms = 148, occ = 0;
 };
 static FusedInfo g_fused[64];
-constexpr size_t kSelDynSmem = (size_t)kSelCache * sizeof(uint64_t) + (size_t)kSelHistWords * sizeof(uint32_t);
+constexpr size_t kSelDynSmem =
+    (size_t)kSelCache * sizeof(uint64_t) + (size_t)(kSelHistWords + kSelMapWords) * sizeof(uint32_t);
 
 static const FusedInfo& fused_info() {
   int dev = 0;
@@ -850,9 +899,10 @@ static bool metrics_fused_batch(const double* ylt, uint64_t n, int mq, const uin
   SelQueries Q;
   memset(&Q, 0, sizeof Q);
   for (int q = 0; q < mq; ++q) Q.k[q] = ks[q];
-  if (!zeroed && (*err = cudaMemsetAsync(st, 0, sizeof(SelScratch), s)) != cudaSuccess) return true;
+  if (!zeroed && (*err = cudaMemsetAsync(st, 0, kSelZeroBytes, s)) != cudaSuccess) return true;
   int m_ = mq;
-  void* args[] = {(void*)&ylt, (void*)&n, (void*)&m_, (void*)&st, (void*)&Q, (void*)&pml_dev, (void*)&tvar_dev};
+  int trace = getenv("ARA_METRICS_TRACE") ? 1 : 0;  // development aid: per-block phase timestamps
+  void* args[] = {(void*)&ylt, (void*)&n, (void*)&m_, (void*)&st, (void*)&Q, (void*)&pml_dev, (void*)&tvar_dev, &trace};
   const bool cached = (n + grid - 1) / grid <= (uint64_t)kSelCache;  // every block's chunk fits its key cache
   *err = cudaLaunchCooperativeKernel(cached ? (const void*)metrics_select<true> : (const void*)metrics_select<false>,
                                      dim3((unsigned)grid), dim3(kSelThreads), args, kSelDynSmem, s);
