@@ -153,9 +153,12 @@ ARA_API ara_status ara_check(ara_ctx* ctx, void* stream);
 
 /* Probable Maximum Loss and Tail Value-at-Risk of a DEVICE YLT of n values >= 0 at m return periods
  * (readings c11, c12, c14): k = ceil(n / RP) -- exact integer ceil for integral RP, ceil(x - 1e-9 x),
- * x = n / RP, otherwise; PML = k-th largest value; TVaR = mean of the k largest.  Computed with a
- * device MSD radix select on the fp64 bit patterns plus a deterministic fp64 tail sum.  Results to
- * HOST out arrays of m doubles; synchronises `stream`.
+ * x = n / RP, otherwise; PML = k-th largest value; TVaR = mean of the k largest.  Computed with one
+ * cooperative launch of a device MSD radix select on the fp64 bit patterns (a 16-bit pass, 12-bit passes
+ * only while a query's bucket holds > 256 values, then compaction; ranks on the maximum/minimum tie
+ * blocks resolve after the first pass) plus a deterministic fp64 sum: results are bitwise reproducible
+ * and, for integer-valued YLTs, bitwise equal to the sorted definition.  Results to HOST out arrays of m
+ * doubles; synchronises `stream`.  NaN values are not supported (their order is undefined).
  * Errors: ARA_E_ARG (NULL, n == 0, m == 0 or m > ARA_MAX_RETURN_PERIODS), ARA_E_RANGE (RP not in
  * (1, n] or not finite), ARA_E_NOMEM, ARA_E_CUDA. */
 ARA_API ara_status ara_pml_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_out,

@@ -313,11 +313,27 @@ def test_run_host_matches_device_path(cuda_device):
 
 
 # ------------------------------------------------------------------ metrics kernels
-@pytest.mark.parametrize("case", ["ties", "uniform", "small", "negzero", "many_rps", "one"])
+@pytest.mark.parametrize("case", ["ties", "uniform", "small", "negzero", "many_rps", "one", "interior_ties",
+                                  "dense_bucket", "all_equal", "signed", "two_values"])
 def test_metrics_match_oracle(cuda_device, case):
+    """metrics_select paths: ranks on the global max/min tie blocks (resolved after the first pass), buckets
+    compacted at 16 or 28 bits, interior tie blocks and dense buckets that need every 12-bit pass down to
+    the full 64-bit key, negative values, the uncached (n > 8192 per block) path."""
     rng = np.random.default_rng(11)
     rps = [2.0, 5.0, 10.0, 20.0, 25.0, 50.0, 100.0, 200.0, 250.0, 500.0, 1000.0]
-    if case == "ties":
+    if case == "interior_ties":  # 40% of the values equal one interior value: the median falls inside it
+        y = np.floor(rng.exponential(1e6, 300_000))
+        y[rng.random(300_000) < 0.4] = 777_777.0
+    elif case == "dense_bucket":  # 200k values within 2^-30 relative of each other (distinct): 64-bit passes
+        y = 1e6 + np.arange(200_000, dtype=np.float64) * (1e6 * 2.0 ** -40)
+        rng.shuffle(y)
+    elif case == "all_equal":
+        y = np.full(123_457, 42.5)
+    elif case == "signed":  # integer-valued, both signs
+        y = np.floor(rng.normal(0.0, 1e5, 400_000))
+    elif case == "two_values":
+        y = np.where(rng.random(250_000) < 0.5, 3.0, 7.0)
+    elif case == "ties":
         y = np.floor(rng.exponential(1000.0, 100_000)) * (rng.random(100_000) > 0.3)
         y[rng.random(100_000) < 0.2] = 4000.0
     elif case == "uniform":
@@ -342,7 +358,7 @@ def test_metrics_match_oracle(cuda_device, case):
     p, t = ara.ara_pml_tvar(d, rps)
     assert np.array_equal(p, oracle.pml(y, rps))
     assert np.all(within_tol(t, oracle.tvar(y, rps), rel=1e-12, abs_floor=1e-9))
-    if case in ("ties", "small", "negzero"):  # integer-valued: exact
+    if case in ("ties", "small", "negzero", "interior_ties", "signed", "two_values"):  # integer-valued: exact
         assert np.array_equal(t, oracle.tvar(y, rps))
     assert np.array_equal(ara.ara_pml(d, rps), p) and np.array_equal(ara.ara_tvar(d, rps), t)
     p2, t2 = ara.ara_pml_tvar(d, rps)
