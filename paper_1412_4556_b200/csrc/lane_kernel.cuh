@@ -267,9 +267,18 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_lane_kernel(const __grid_const
     }
     pw0 = pw1 = pw2 = pw3 = z2;
   };
-  auto flush_pending = [&]() {  // XS: every pending window, oldest first
+  // XS: every pending window, oldest first.  A window adds up to 4 entries per lane and a queue holds 8, so
+  // with two pending windows the queue must be drained to <= 4 entries between them (without this a lane
+  // could overflow its queue at a trial's end and lose a hit: measured on config X's real-regime YLT)
+  auto drain_to_4 = [&]() {
+    while (__any_sync(FULL, tail - head >= (kLaneQ - 3u) * 128u)) round();
+  };
+  auto flush_pending = [&]() {
     flush_oldest();
-    if constexpr (XD == 2) flush_oldest();
+    if constexpr (XD == 2) {
+      drain_to_4();
+      flush_oldest();
+    }
   };
   auto scan = [&](const uint4 v, uint32_t valid) {
     if constexpr (XS) {

@@ -270,6 +270,32 @@ def test_exact_scan_filter_compact_records_dense(cuda_device):
     ctx.close()
 
 
+def test_exact_scan_filter_full_queues(cuda_device):
+    """Every id of the catalogue holds a loss (each lane queues a hit for every slot of every window): the
+    lane queues run full at every trial end, where the two-window deferral (XS2) flushes two pending windows
+    (8 entries per lane) -- the queue must be drained between them.  Every XS variant equals the oracle
+    bitwise (integer regime)."""
+    C, J, K, N = 2048, 4, 1000, 700
+    rng = np.random.default_rng(29)
+    elts = []
+    for j in range(J):
+        ids = np.arange(1, C + 1, dtype=np.uint32) if j == 0 else np.unique(rng.integers(1, C + 1, size=700)).astype(np.uint32)
+        rng.shuffle(ids)
+        elts.append((ids, rng.integers(1, 1 << 20, size=ids.size).astype(np.float32), (float(rng.integers(0, 1 << 12)), float(1 << 21))))
+    layer = (list(range(J)), (3000.0, float(1 << 24)), (1e5, 4e9))
+    yet = rng.integers(1, C + 1, size=N * K).astype(np.uint32)
+    want = oracle.ylt(C, yet, None, N, K, elts, [layer])
+    ctx = _ctx(C, elts, [layer])
+    ctx.ara_set_option(ara.ARA_OPT_FILTER, 1)
+    for v in (4, 5, 6, 7):  # XS 24, XS2 24, XS 32/16 warps
+        ctx.ara_set_option(ara.ARA_OPT_KERNEL, ara.KERNEL_PRESENCE)
+        ctx.ara_set_option(ara.ARA_OPT_STREAM, v + 1)
+        got = gpu_ylt(None, ctx, yet, K=K, num_trials=N)
+        assert ",XS" in ctx.ara_kernel_name(), ctx.ara_kernel_name()
+        assert np.array_equal(got, want), v
+    ctx.close()
+
+
 def test_exact_scan_filter_config_x_sampled(cuda_device):
     """Config X itself (real regime) on a 20,000-trial slice generated on the device: the automatic
     kernel (lane + exact scan filter) within tolerance of the oracle on 500 sampled trials and of the
