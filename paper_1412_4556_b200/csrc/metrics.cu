@@ -379,13 +379,19 @@ __device__ __forceinline__ void merge_min(uint64_t& v, uint32_t& c, uint64_t v2,
   v = v2 < v ? v2 : v;
 }
 __device__ __forceinline__ void warp_merge_extremes(uint64_t& mx, uint32_t& cx, uint64_t& mn, uint32_t& cn) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const uint64_t a = __shfl_xor_sync(0xffffffffu, mx, off), b = __shfl_xor_sync(0xffffffffu, mn, off);
-    const uint32_t ca = __shfl_xor_sync(0xffffffffu, cx, off), cb = __shfl_xor_sync(0xffffffffu, cn, off);
-    merge_max(mx, cx, a, ca);
-    merge_min(mn, cn, b, cb);
-  }
+  // warp reductions (REDUX) on the 32-bit halves: the high words, then the low words among the lanes that
+  // hold the extreme high word, then the multiplicities of the extreme key
+  const unsigned FULL = 0xffffffffu;
+  const uint32_t hx = __reduce_max_sync(FULL, (uint32_t)(mx >> 32));
+  const uint32_t lx = __reduce_max_sync(FULL, (uint32_t)(mx >> 32) == hx ? (uint32_t)mx : 0u);
+  const uint64_t gx = ((uint64_t)hx << 32) | lx;
+  cx = __reduce_add_sync(FULL, mx == gx ? cx : 0u);
+  mx = gx;
+  const uint32_t hn = __reduce_min_sync(FULL, (uint32_t)(mn >> 32));
+  const uint32_t ln = __reduce_min_sync(FULL, (uint32_t)(mn >> 32) == hn ? (uint32_t)mn : 0xffffffffu);
+  const uint64_t gn = ((uint64_t)hn << 32) | ln;
+  cn = __reduce_add_sync(FULL, mn == gn ? cn : 0u);
+  mn = gn;
 }
 
 // Index of the slot whose key range [slo, shi] holds `key` among `ns` disjoint ranges sorted by slo, else -1.
@@ -446,7 +452,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
   __shared__ int s_nbits[kMaxQ], s_mode[kMaxQ], s_q2slot[kMaxQ], s_nslot;
   __shared__ unsigned long long s_ev[2][32];
   __shared__ uint32_t s_ec[2][32];
-  __shared__ double wsum[kSelThreads / 32][kMaxQ];
   const unsigned FULL = 0xffffffffu;
   const unsigned nb = gridDim.x;
   const uint64_t lo = n * blockIdx.x / nb, hi = n * (blockIdx.x + 1) / nb;
@@ -702,8 +707,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
     const int rb = 64 - s_nbits[q];
     s_up[q] = s_mode[q] == kModeDone ? s_T[q] : ((s_pre[q] << rb) | ((1ull << rb) - 1ull));
   }
+  for (uint32_t i = threadIdx.x; i < 2048u; i += blockDim.x) smap[i] = 0u;  // 16-bit prefixes of the buckets
   __syncthreads();
   const int nc = s_nslot;
+  if (threadIdx.x < (unsigned)nc) {  // every candidate bucket holds >= 16 bits: its top 16 bits are one prefix
+    const uint32_t d = (uint32_t)(s_slo[threadIdx.x] >> 48);
+    atomicOr(&smap[d >> 5], 1u << (d & 31u));
+  }
+  __syncthreads();
   if (nc > 0) {  // block-local lists in shared memory, then copied to this block's region (no global atomics)
     uint64_t* lc = reinterpret_cast<uint64_t*>(hw);  // [nc][kCandCap]
     __shared__ uint32_t s_ln[kMaxQ];
@@ -712,7 +723,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
     const uint64_t rlo = s_slo[0], rhi = s_shi[nc - 1];
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
       const uint64_t key = key_at(i);
-      if (key >= rlo && key <= rhi) {
+      const uint32_t d = (uint32_t)(key >> 48);
+      if (key >= rlo && key <= rhi && ((smap[d >> 5] >> (d & 31u)) & 1u)) {  // most keys stop at the map
         const int sl = find_range(key, s_slo, s_shi, nc);
         if (sl >= 0) lc[sl * kCandCap + atomicAdd(&s_ln[sl], 1u)] = key;
       }
@@ -725,37 +737,56 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
     }
   }
   stamp();
-  // fp64 sums of the values above s_up, eight queries per sweep (fixed thread order; counts are known)
-  for (int q0 = 0; q0 < m; q0 += 8) {
-    uint64_t up[8];
-    double a[8];
+  // fp64 sums of the values above s_up: every key adds its value to ONE interval between consecutive
+  // thresholds (ascending: query s_ord[i] has the i-th smallest), in a per-thread column of shared memory;
+  // the intervals are reduced in a fixed order and each query takes the suffix sum of the intervals above
+  // its threshold -- one fp64 add per key instead of one per (key, query); counts follow from the ranks.
+  __shared__ uint64_t s_uo[kMaxQ];
+  __shared__ int s_ord[kMaxQ];
+  if (w == 0 && lane < m) {
+    const uint64_t u = s_up[lane];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) rank += (s_up[j] < u || (s_up[j] == u && j < lane)) ? 1 : 0;
+    s_uo[rank] = u;
+    s_ord[rank] = lane;
+  }
+  __syncthreads();  // (the compaction above is done with hw)
+  double* bk = reinterpret_cast<double*>(hw);  // [kMaxQ][kSelThreads]: interval i of this thread
+  for (int i = 0; i < m; ++i) bk[i * kSelThreads + threadIdx.x] = 0.0;
+  __syncthreads();
+  {
+    const uint64_t u0 = s_uo[0];
+    for (uint32_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const uint64_t key = key_at(e);
+      if (key > u0) {  // the largest i with s_uo[i] < key
+        int i = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      up[j] = q0 + j < m ? s_up[q0 + j] : ~0ull;  // no key exceeds ~0
-      a[j] = 0.0;
-    }
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-      const uint64_t key = key_at(i);
-      const double v = from_key(key);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (key > up[j]) a[j] += v;
-    }
-    stamp();
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (q0 + j < m) {  // warp-uniform
-        double aj = a[j];
-        for (int off = 16; off > 0; off >>= 1) aj += __shfl_xor_sync(FULL, aj, off);
-        if (lane == 0) wsum[w][q0 + j] = aj;
+        for (int step = 8; step > 0; step >>= 1)
+          if (i + step < m && s_uo[i + step] < key) i += step;
+        bk[i * kSelThreads + threadIdx.x] += from_key(key);
       }
     }
   }
+  stamp();
   __syncthreads();
-  if (threadIdx.x < (unsigned)m) {
+  __shared__ double s_bsum[kMaxQ];
+  if (w < m) {  // warp i reduces interval i: lane l sums threads 32l .. 32l+31 in order, then a fixed tree
+    const double* col = bk + w * kSelThreads + 32 * lane;
     double a = 0.0;
-    for (int i = 0; i < kSelThreads / 32; ++i) a += wsum[i][threadIdx.x];
-    S->psum[blockIdx.x][threadIdx.x] = a;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) a += col[(t + lane) & 31];  // rotated start: no bank conflicts; fixed per lane
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
+    if (lane == 0) s_bsum[w] = a;
+  }
+  __syncthreads();
+  if (w == 0) {
+    if (lane == 0) {  // query s_ord[i] sums the intervals i .. m-1, added from the top interval down
+      double acc = 0.0;
+      for (int i = m - 1; i >= 0; --i) {
+        acc += s_bsum[i];
+        S->psum[blockIdx.x][s_ord[i]] = acc;
+      }
+    }
   }
   stamp();
   grid_sync(&S->bar_count, bar_target += nb);

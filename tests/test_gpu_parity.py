@@ -314,14 +314,17 @@ def test_run_host_matches_device_path(cuda_device):
 
 # ------------------------------------------------------------------ metrics kernels
 @pytest.mark.parametrize("case", ["ties", "uniform", "small", "negzero", "many_rps", "one", "interior_ties",
-                                  "dense_bucket", "all_equal", "signed", "two_values"])
+                                  "dense_bucket", "all_equal", "signed", "two_values", "large"])
 def test_metrics_match_oracle(cuda_device, case):
     """metrics_select paths: ranks on the global max/min tie blocks (resolved after the first pass), buckets
     compacted at 16 or 28 bits, interior tie blocks and dense buckets that need every 12-bit pass down to
     the full 64-bit key, negative values, the uncached (n > 8192 per block) path."""
     rng = np.random.default_rng(11)
     rps = [2.0, 5.0, 10.0, 20.0, 25.0, 50.0, 100.0, 200.0, 250.0, 500.0, 1000.0]
-    if case == "interior_ties":  # 40% of the values equal one interior value: the median falls inside it
+    if case == "large":  # > 65,535 keys per block: histograms built in sub-chunks, keys re-read from HBM
+        y = np.floor(rng.exponential(1e6, 10_000_019)) * (rng.random(10_000_019) > 0.2)
+        rps = [2.0, 10.0, 100.0, 1000.0, 10000.0, 1e6]
+    elif case == "interior_ties":  # 40% of the values equal one interior value: the median falls inside it
         y = np.floor(rng.exponential(1e6, 300_000))
         y[rng.random(300_000) < 0.4] = 777_777.0
     elif case == "dense_bucket":  # 200k values within 2^-30 relative of each other (distinct): 64-bit passes
@@ -358,7 +361,7 @@ def test_metrics_match_oracle(cuda_device, case):
     p, t = ara.ara_pml_tvar(d, rps)
     assert np.array_equal(p, oracle.pml(y, rps))
     assert np.all(within_tol(t, oracle.tvar(y, rps), rel=1e-12, abs_floor=1e-9))
-    if case in ("ties", "small", "negzero", "interior_ties", "signed", "two_values"):  # integer-valued: exact
+    if case in ("ties", "small", "negzero", "interior_ties", "signed", "two_values", "large"):  # integer-valued: exact
         assert np.array_equal(t, oracle.tvar(y, rps))
     assert np.array_equal(ara.ara_pml(d, rps), p) and np.array_equal(ara.ara_tvar(d, rps), t)
     p2, t2 = ara.ara_pml_tvar(d, rps)

@@ -322,6 +322,41 @@ def test_exact_scan_filter_config_x_sampled(cuda_device):
     assert np.all(within_tol(got[:, sample], want))
 
 
+@pytest.mark.parametrize("name", ["P", "X"])
+def test_variant_groups_bitwise_real_regime(cuda_device, name):
+    """Every kernel family on a 20,000-trial slice of a real-regime configuration (device-generated YET):
+    kernels that share a summation order agree BIT FOR BIT -- {presence, warp ring}, {every lane-queue and
+    exact-filter variant}, {the two mask variants} -- and every family is within the north_star tolerance
+    of the oracle on sampled trials.  (A lost hit in one variant showed up only here: integer-regime tests
+    on small shapes had passed.)"""
+    cfg = synth.Config.load(name)
+    elts = synth.make_elts(cfg)
+    N, K = 20_000, cfg.kmin
+    ids = torch.empty(N * K, dtype=torch.int32, device=cuda_device)
+    synth.yet_ids_device(ids.data_ptr(), cfg.seed, cfg.catalog_size, 0, N * K, torch.cuda.current_stream().cuda_stream)
+    ctx = ara.context_for_config(cfg, elts)
+
+    def run(kernel, v=0):
+        select(ctx, kernel, v)
+        y = torch.full((1, N), -1.0, dtype=torch.float64, device=cuda_device)
+        ctx.ara_run(ids, y, events_per_trial=K, num_trials=N)
+        ctx.ara_check()
+        return ctx.ara_kernel_name(), y.cpu().numpy()
+
+    groups = {"presence": [run(ara.KERNEL_PRESENCE, 0), run(KERNEL_STREAM, RING_VARIANT)],
+              "lane": [run(KERNEL_STREAM, v) for v in LANE_VARIANTS + (4, 5, 6, 7)],
+              "mask": [run(KERNEL_STREAM, v) for v in MASK_VARIANTS]}
+    sample = np.arange(0, N, 100)
+    want = oracle.ylt_for(cfg, elts, synth.make_yet_trials(cfg, sample))
+    for g, runs in groups.items():
+        first_name, first = runs[0]
+        for kname, y in runs[1:]:
+            assert np.array_equal(y, first), (g, first_name, kname, int((y != first).sum()))
+        assert np.all(within_tol(first[:, sample], want)), g
+        assert np.all(within_tol(first, groups["presence"][0][1])), g
+    ctx.close()
+
+
 # ------------------------------------------------------------------ SURVEY N1: fused multi-layer pass
 def _layers_distinct(J_list, C, seed, integer=True, shared=False, n=800):
     """Layers over distinct ELTs (config M's reading c20), or all over the same ELTs (`shared`, the tower)."""
