@@ -51,7 +51,7 @@ def parse():
                     help="ARA_OPT_FILTER: exact filter stage of the record presence kernel (-1 auto)")
     ap.add_argument("--stream", type=int, default=None,
                     help="ARA_OPT_STREAM: 0 = presence kernel for fixed-length trials, 1..3 = stream kernel variant")
-    ap.add_argument("--prefetch", type=int, default=None, choices=[-1, 0, 1, 2], help="ARA_OPT_PREFETCH")
+    ap.add_argument("--prefetch", type=int, default=None, choices=[-1, 0, 1], help="ARA_OPT_PREFETCH")
     ap.add_argument("--round-min", type=int, default=None, help="ARA_OPT_ROUND_MIN (lane kernel round trigger)")
     ap.add_argument("--trial-order", type=int, default=None, choices=[0, 1], help="ARA_OPT_TRIAL_ORDER")
     ap.add_argument("--fused", type=int, default=None, choices=[0, 1], help="ARA_OPT_FUSED (multi-layer single pass)")

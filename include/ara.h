@@ -230,9 +230,7 @@ ARA_API ara_status ara_unshard(const double* gathered, uint32_t num_shards, uint
  *                           (default: on for the per-lane-queue and warp-ring kernels -- one bulk
  *                           prefetch of the trial after next per trial --, off for the presence and
  *                           candidate-mask kernels), 0 off, 1 on
- *                           (presence kernel: each warp prefetches its next trial at a trial start),
- *                           2 presence kernel only: every window prefetches the window two loads
- *                           ahead (one prefetch.global.L2 per 128-B line)
+ *                           (presence kernel: each warp prefetches its next trial at a trial start)
  *   ARA_OPT_VARIANT         kernel variant index within the selected kernel and row width
  *                           (ara_layer_info reports the count)
  *   ARA_OPT_KERNEL          -1 auto (default): per layer, the presence kernel when its folded bitmap is

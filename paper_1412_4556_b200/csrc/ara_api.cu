@@ -545,7 +545,7 @@ static ara_status launch_layer(ara_ctx* c, Layer& L, const uint32_t* ids, const 
   p.C = c->C;
   p.jpad = L.jpad;
   p.l2_hints = c->l2_policy == 1 ? 0u : 1u;
-  p.prefetch = c->prefetch > 0 ? (uint32_t)c->prefetch : 0u;  // presence: 1 next trial, 2 every window
+  p.prefetch = c->prefetch > 0 ? 1u : 0u;
   p.ylt = ylt;
   p.olt = olt;
   p.err = c->d_err;
@@ -1472,7 +1472,7 @@ ara_status ara_set_option(ara_ctx* c, ara_option opt, int64_t v) {
       c->variant = 0;
       return ARA_OK;
     case ARA_OPT_PREFETCH:
-      if (v < -1 || v > 2) return set_error(ARA_E_ARG, "prefetch in {-1, 0, 1, 2}");
+      if (v < -1 || v > 1) return set_error(ARA_E_ARG, "prefetch in {-1, 0, 1}");
       c->prefetch = (int)v;
       return ARA_OK;
     case ARA_OPT_FILTER:

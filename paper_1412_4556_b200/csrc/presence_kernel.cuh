@@ -302,7 +302,6 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
   const uint32_t C = p.C;
   const uint32_t fmul = p.fold_mul;
   const unsigned lt = lanemask_lt();
-  const bool pf_win = p.prefetch == 2u && (lane & 7) == 0;  // per-window L2 prefetch (option)
 
   double S0 = 0.0, S1 = 0.0;  // per-lane partial sums of the (<= 2) open trials, by parity
   double M0 = 0.0, M1 = 0.0;  // per-lane largest occurrence-net loss of those trials (OLT)
@@ -501,7 +500,7 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
 
     // Bring this warp's NEXT trial into L2 (lane l prefetches its 128-B line l: the first 4 KB), so its
     // windows arrive at L2 latency: one window of register prefetch cannot cover DRAM latency.
-    if (p.prefetch == 1u) {
+    if (p.prefetch) {
       const uint64_t tn = t + (uint64_t)gridDim.x * NW;
       if (tn < p.num_trials) {
         const uint64_t nb = p.offsets ? p.offsets[tn] : tn * p.K;
@@ -539,8 +538,6 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
         while (true) {
           ok_b = r + 128u < len;
           if (rem != 0u && ok_b) wb = ld_ids4_stream(lpp + 128);
-          // ARA_OPT_PREFETCH 2: the first lane of each 128-B line pulls the window two loads ahead into L2
-          if (pf_win && r + 384u < len) prefetch_l2_line(lpp + 384);
           scan(wa, BoolC<false>{}, 0u, 0u, ok_a ? 0xffffffffu : 0u);
           if (rem == 0u) break;
           --rem;
@@ -548,7 +545,6 @@ __global__ void __launch_bounds__(NW * 32, 1) ara_presence_kernel(const __grid_c
           r += 256u;
           ok_a = r < len;
           if (rem != 0u && ok_a) wa = ld_ids4_stream(lpp);
-          if (pf_win && r + 256u < len) prefetch_l2_line(lpp + 256);
           scan(wb, BoolC<false>{}, 0u, 0u, ok_b ? 0xffffffffu : 0u);
           if (rem == 0u) break;
           --rem;
