@@ -317,8 +317,7 @@ ARA_API ara_status ara_layer_stats(ara_ctx* ctx, uint32_t layer, uint64_t* prese
  * its last layer (a static string; "" before the first run). */
 ARA_API const char* ara_kernel_name(ara_ctx* ctx);
 
-/* Test hook: copy row `event` of layer l's table (row_stride bytes) to HOST out.  Synchronous. */
-ARA_API ara_status ara_table_row(ara_ctx* ctx, uint32_t layer, uint32_t event, float* out);
+/* (The test-only table read-back, ara_table_row, lives in libara_testing.so: include/ara_testing.h.) */
 
 ARA_API const char* ara_status_string(ara_status s);
 ARA_API const char* ara_last_error(void);

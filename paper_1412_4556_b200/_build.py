@@ -2,6 +2,7 @@
 
     libara.so        the product: C ABI of include/ara.h (csrc/*.cu)
     libara_synth.so  the seeded device input generator (synth/synth.cu; test/bench infrastructure)
+    libara_testing.so  test-only read-back of a context's tables (csrc/testing.cu, include/ara_testing.h)
 """
 from __future__ import annotations
 
@@ -22,13 +23,16 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
 LIBS = {
     "libara.so": [os.path.join(HERE, "csrc", f) for f in ("ara_api.cu", "metrics.cu", "kernels_presence.cu", "kernels_presence_mid.cu", "kernels_presence_wide.cu", "kernels_dense.cu", "kernels_study.cu", "outputs.cu", "kernels_stream.cu")],
     "libara_synth.so": [os.path.join(HERE, "synth", "synth.cu")],
+    "libara_testing.so": [os.path.join(HERE, "csrc", "testing.cu")],
 }
 DEPS = {
     # every header under csrc/ (a kernel header missing here once left a stale libara.so in place)
     "libara.so": sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(INCLUDE, "ara.h")],
     "libara_synth.so": [os.path.join(INCLUDE, "ara_synth.h")],
+    "libara_testing.so": sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(INCLUDE, "ara.h"),
+                                                                                 os.path.join(INCLUDE, "ara_testing.h")],
 }
-OUT_DIR = {"libara.so": HERE, "libara_synth.so": os.path.join(HERE, "synth")}
+OUT_DIR = {"libara.so": HERE, "libara_synth.so": os.path.join(HERE, "synth"), "libara_testing.so": HERE}
 
 
 def _stale(out, srcs):

@@ -37,7 +37,7 @@ ARA_MAX_ELTS_PER_LAYER = 128
 EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_ex", "ara_run_host", "ara_run_study", "ara_aal", "ara_ep",
            "ara_sum_layers", "ara_check", "ara_pml_tvar", "ara_pml",
            "ara_tvar", "ara_pml_tvar_device", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
-           "ara_layer_info", "ara_layer_stats", "ara_table_row", "ara_kernel_name", "ara_status_string", "ara_last_error",
+           "ara_layer_info", "ara_layer_stats", "ara_kernel_name", "ara_status_string", "ara_last_error",
            "ara_version", "ara_plan_create", "ara_plan_launch", "ara_plan_destroy")
 
 
@@ -101,7 +101,6 @@ def lib() -> ctypes.CDLL:
                                     ctypes.POINTER(ctypes.c_char_p)]),
             "ara_layer_stats": (st, [vp, u32, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_int)]),
-            "ara_table_row": (st, [vp, u32, u32, dp]),
             "ara_kernel_name": (ctypes.c_char_p, [vp]),
             "ara_plan_create": (st, [vp, ctypes.POINTER(_Yet), dp, dp, u32, dp, dp, vp, ctypes.POINTER(vp)]),
             "ara_plan_launch": (st, [vp, vp]),
@@ -116,6 +115,27 @@ def lib() -> ctypes.CDLL:
             f.argtypes = args
         _lib = L
     return _lib
+
+
+TESTING_LIB_PATH = os.path.join(_HERE, "libara_testing.so")
+TESTING_EXPORTS = ("ara_table_row", "ara_testing_last_error")
+_tlib = None
+
+
+def testing_lib() -> ctypes.CDLL:
+    """Load the test-only libara_testing.so (include/ara_testing.h); libara.so is loaded first."""
+    global _tlib
+    if _tlib is None:
+        lib()
+        if not os.path.exists(TESTING_LIB_PATH):
+            raise RuntimeError(f"{TESTING_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        T = ctypes.CDLL(TESTING_LIB_PATH)
+        T.ara_table_row.restype = ctypes.c_int
+        T.ara_table_row.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p]
+        T.ara_testing_last_error.restype = ctypes.c_char_p
+        T.ara_testing_last_error.argtypes = []
+        _tlib = T
+    return _tlib
 
 
 def _status_name(s: int) -> str:
@@ -305,9 +325,13 @@ class Context:
         return lib().ara_kernel_name(self._h).decode()
 
     def ara_table_row(self, layer: int, event: int) -> np.ndarray:
+        """Test hook (libara_testing.so, include/ara_testing.h): row `event` of layer `layer`'s table."""
         stride = self.ara_layer_info(layer)["row_stride"]
         out = np.zeros(stride // 4, dtype=np.float32)
-        _check(lib().ara_table_row(self._h, layer, event, _dptr(out)), "ara_table_row")
+        T = testing_lib()
+        st = T.ara_table_row(self._h, layer, event, _dptr(out))
+        if st != ARA_OK:
+            raise AraError(st, "ara_table_row", T.ara_testing_last_error().decode())
         return out
 
 

@@ -32,6 +32,18 @@ def test_library_exports_every_declared_symbol():
     assert exported == _declared()
 
 
+def test_testing_library_exports_its_header():
+    """Test hooks live in libara_testing.so (include/ara_testing.h), not in the product ABI."""
+    txt = open(os.path.join(ROOT, "include", "ara_testing.h")).read()
+    declared = sorted(set(re.findall(r"ARA_API\s+[\w\s\*]+?\b(ara_\w+)\s*\(", txt)))
+    assert declared == sorted(ara.TESTING_EXPORTS)
+    out = subprocess.run(["nm", "-D", "--defined-only", ara.TESTING_LIB_PATH], capture_output=True, text=True).stdout
+    assert sorted(l.split()[-1] for l in out.splitlines() if " T " in l) == declared
+    assert "ara_table_row" not in _declared()
+    T = ara.testing_lib()
+    assert T.ara_table_row(None, 0, 0, None) == ara.ARA_E_ARG
+
+
 def test_synth_library_exports():
     out = subprocess.run(["nm", "-D", "--defined-only",
                           os.path.join(ROOT, "paper_1412_4556_b200", "synth", "libara_synth.so")],
