@@ -1,8 +1,7 @@
 """Print the device/host facts the design depends on (L2 size, persisting limits, SM count, host cores)."""
-import ctypes, os, json, subprocess
+import os, json, subprocess
 import torch
 p = torch.cuda.get_device_properties(0)
-cudart = ctypes.CDLL("libcudart.so.12") if False else None
 out = {"name": p.name, "sms": p.multi_processor_count, "l2": getattr(p, "L2_cache_size", None),
        "mem": p.total_memory, "cc": [p.major, p.minor], "host_cores": os.cpu_count()}
 try:
