@@ -4,18 +4,6 @@
 
 namespace ara {
 
-#define ARA_PRES(V_, NV_, G_, NW_) \
-  {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, G_, 0, NW_, ara_presence_kernel<V_, NV_, G_, NW_, false>, \
-   "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",NW=" #NW_ ">", ara_presence_kernel<V_, NV_, G_, NW_, true>}
-// default one-lane-per-row variant, also instantiated with the exact filter stage (FX) and with the
-// precombined occurrence-net table (PC)
-#define ARA_PRES_FX(V_, NV_, NW_) \
-  {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, 1, 0, NW_, ara_presence_kernel<V_, NV_, 1, NW_, false>, \
-   "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=1,NW=" #NW_ ">", ara_presence_kernel<V_, NV_, 1, NW_, true>, \
-   ara_presence_kernel<V_, NV_, 1, NW_, false, true>, ara_presence_kernel<V_, NV_, 1, NW_, true, true>, \
-   ara_presence_kernel<V_, NV_, 1, NW_, false, false, true>, ara_presence_kernel<V_, NV_, 1, NW_, true, false, true>}
-
-
 static const Variant kTable[] = {
     // first per row width = default: one lane per row with sparse records (G = 1); then full-row batches
     ARA_PRES_FX(8, 3, 32), ARA_PRES(8, 3, 2, 16), ARA_PRES(8, 3, 4, 16), ARA_PRES(8, 3, 2, 24),

@@ -41,4 +41,17 @@ struct StreamVariant {
 };
 const StreamVariant* stream_variants(int* n);  // kernels_stream.cu; first = default
 
+// Variant-table entries of the presence kernel (presence_kernel.cuh; used by the kernels_presence*.cu
+// instantiation tables).  ARA_PRES: one (V, NV, G, NW) shape with and without the occurrence loss table.
+// ARA_PRES_FX: the default one-lane-per-row shape of a row width, also instantiated with the exact filter
+// stage (FX) and the precombined occurrence-net table (PC).
+#define ARA_PRES(V_, NV_, G_, NW_) \
+  {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, G_, 0, NW_, ara_presence_kernel<V_, NV_, G_, NW_, false>, \
+   "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=" #G_ ",NW=" #NW_ ">", ara_presence_kernel<V_, NV_, G_, NW_, true>}
+#define ARA_PRES_FX(V_, NV_, NW_) \
+  {KIND_PRESENCE, (uint32_t)((V_) * (NV_)), V_, NV_, 1, 0, NW_, ara_presence_kernel<V_, NV_, 1, NW_, false>, \
+   "ara_presence_kernel<V=" #V_ ",NV=" #NV_ ",G=1,NW=" #NW_ ">", ara_presence_kernel<V_, NV_, 1, NW_, true>, \
+   ara_presence_kernel<V_, NV_, 1, NW_, false, true>, ara_presence_kernel<V_, NV_, 1, NW_, true, true>, \
+   ara_presence_kernel<V_, NV_, 1, NW_, false, false, true>, ara_presence_kernel<V_, NV_, 1, NW_, true, false, true>}
+
 }  // namespace ara
