@@ -39,6 +39,8 @@ def t(**opt):
 
 
 base = t(stream=0, prefetch=-1, trial_order=1, round_min=24)
+if os.environ.get("X_SWEEP_BASE_ONLY"):
+    sys.exit(0)
 for extra in [dict(stream=5), dict(stream=6), dict(stream=7), dict(stream=8),
               dict(stream=5, round_min=16), dict(stream=5, round_min=20), dict(stream=5, round_min=28),
               dict(stream=5, round_min=24, prefetch=0), dict(stream=5, prefetch=1, trial_order=0)]:
