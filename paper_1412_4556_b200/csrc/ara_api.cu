@@ -803,6 +803,7 @@ ara_status ara_table_footprint(uint32_t catalog_size, uint32_t num_elts, uint64_
 
 ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_elts, const ara_layer* layers,
                       uint32_t num_layers, int device, void* stream, ara_ctx** out) {
+  ara::NvtxRange nvtx("ara_create");
   if (!out) return set_error(ARA_E_ARG, "out is NULL");
   *out = nullptr;
   ara_status st = validate(catalog_size, elts, num_elts, layers, num_layers);
@@ -981,6 +982,7 @@ ara_status ara_create(uint32_t catalog_size, const ara_elt* elts, uint32_t num_e
 void ara_destroy(ara_ctx* ctx) { destroy_ctx(ctx); }
 
 ara_status ara_run_ex(ara_ctx* c, const ara_yet* yet, double* ylt, double* olt, void* stream) {
+  ara::NvtxRange nvtx("ara_run");
   if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
   ara_status st = check_yet(yet);
   if (st) return st;
@@ -1087,6 +1089,7 @@ ara_status ara_plan_create(ara_ctx* c, const ara_yet* yet, double* ylt, const do
 }
 
 ara_status ara_plan_launch(ara_plan* p, void* stream) {
+  ara::NvtxRange nvtx("ara_plan_launch");
   if (!p || !p->exec) return set_error(ARA_E_ARG, "plan is NULL");
   DeviceGuard guard(p->device);
   ARA_CUDA(cudaGraphLaunch(p->exec, (cudaStream_t)stream));
@@ -1102,6 +1105,7 @@ ara_status ara_check(ara_ctx* c, void* stream) {
 }
 
 ara_status ara_run_host(ara_ctx* c, const ara_yet* yet, double* ylt_host, void* stream) {
+  ara::NvtxRange nvtx("ara_run_host");
   if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
   ara_status st = check_yet(yet);
   if (st) return st;

@@ -4,9 +4,17 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <nvtx3/nvToolsExt.h>  // header-only: a no-op unless a profiler (nsys, ncu) injects itself
+
 #include "ara.h"
 
 namespace ara {
+
+// NVTX range over an ABI call (host timeline annotation for nsys / ncu --nvtx).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 ara_status set_error(ara_status s, const char* fmt, ...);
 ara_status cuda_error(cudaError_t e, const char* what);

@@ -1099,12 +1099,14 @@ extern "C" {
 
 ara_status ara_pml_tvar(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_out,
                         double* tvar_out, void* stream) {
+  ara::NvtxRange nvtx("ara_pml_tvar");
   if (!pml_out && !tvar_out) return ara::set_error(ARA_E_ARG, "no output");
   return ara::metrics(ylt, n, rps, m, pml_out, tvar_out, (cudaStream_t)stream);
 }
 
 ara_status ara_pml_tvar_device(const double* ylt, uint64_t n, const double* rps, uint32_t m, double* pml_dev,
                                double* tvar_dev, void* stream) {
+  ara::NvtxRange nvtx("ara_pml_tvar_device");
   return ara::metrics_device(ylt, n, rps, m, pml_dev, tvar_dev, (cudaStream_t)stream);
 }
 
