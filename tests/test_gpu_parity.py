@@ -48,6 +48,13 @@ def test_table_rows_exhaustive_tiny(cuda_device):
     for e in range(cfg.catalog_size + 1):
         assert np.array_equal(ctx.ara_table_row(0, e), want[e]), e
     assert np.count_nonzero(want == 0) == 2 * (cfg.catalog_size + 1) - 2 * cfg.entries_per_elt
+    # the test-only library's error contract (include/ara_testing.h)
+    with pytest.raises(ara.AraError) as ei:
+        ctx.ara_table_row(0, cfg.catalog_size + 1)
+    assert ei.value.status == ara.ARA_E_RANGE
+    with pytest.raises(ara.AraError) as ei:
+        ctx.ara_table_row(1, 0)
+    assert ei.value.status == ara.ARA_E_ARG
 
 
 # ------------------------------------------------------------------ golden worked examples (bitwise)
