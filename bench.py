@@ -319,6 +319,7 @@ def main():
     # folds set up beforehand), so the timed loop issues one graph launch per step for it; the CUDA events
     # around that launch time the ARA kernels alone.  --eager issues ara_run directly.
     plan = None
+    mplan = [None]  # captured PML/TVaR (ara_metrics_plan_create), set up after the correctness gate
     if not args.eager:
         plan = ctx.ara_plan_create(ids, ylt_local, [], None, None, offsets=offsets_d, events_per_trial=K,
                                    num_trials=n_local, stream=stream)
@@ -340,8 +341,11 @@ def main():
         nvtx.range_push("gather+pml_tvar")
         full = gat.gather(stream=stream) if world > 1 else ylt_local
         if m and (world == 1 or rank == 0):
-            for l in range(L):  # results straight into the rows copied to the host (no device-side copies)
-                ara.ara_pml_tvar_device(full[l], rps, met[l, 0], met[l, 1], stream=stream)
+            if mplan[0] is not None:  # one graph launch: every layer's PML/TVaR into the host-copied rows
+                mplan[0].launch(stream=stream)
+            else:
+                for l in range(L):  # results straight into the rows copied to the host (no device-side copies)
+                    ara.ara_pml_tvar_device(full[l], rps, met[l, 0], met[l, 1], stream=stream)
         nvtx.range_pop()
         if evs is not None:
             evs[2].record(stream)
@@ -357,6 +361,16 @@ def main():
         p_sync, t_sync = ara.ara_pml_tvar(full[l], rps, stream=stream)
         if not (np.array_equal(p_sync, met_h[l, 0].numpy()) and np.array_equal(t_sync, met_h[l, 1].numpy())):
             print(json.dumps({"error": f"layer {l}: ara_pml_tvar_device != ara_pml_tvar"}), flush=True)
+            sys.exit(3)
+    if m and (world == 1 or rank == 0) and not args.eager:  # the captured metric step, checked bit for bit
+        mplan[0] = ara.ara_metrics_plan_create(full, rps, met[:, 0], met[:, 1], out_stride=2 * met.shape[2],
+                                               stream=stream)
+        ref_h = met_h.clone()
+        met.zero_()
+        step()
+        torch.cuda.synchronize()
+        if not torch.equal(met_h, ref_h):
+            print(json.dumps({"error": "captured metric step != ara_pml_tvar_device"}), flush=True)
             sys.exit(3)
     cpu = None
     if not args.profile and not args.no_cpu_baseline:

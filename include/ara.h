@@ -139,6 +139,16 @@ ARA_API ara_status ara_plan_create(ara_ctx* ctx, const ara_yet* yet, double* ylt
                                    double* pml_dev, double* tvar_dev, void* stream, ara_plan** out);
 ARA_API ara_status ara_plan_launch(ara_plan* plan, void* stream);
 ARA_API void ara_plan_destroy(ara_plan* plan); /* NULL is a no-op */
+/* A captured PML/TVaR step (readings c11-c14): the metrics of num_layers DEVICE YLTs of
+ * n values each (layer l at ylt + l * n, borrowed) at the m return periods, recorded once into a CUDA
+ * graph with its scratch allocated and zeroed beforehand (no per-call allocation or memset); layer l's
+ * results go to pml_dev + l * out_stride and tvar_dev + l * out_stride (DEVICE, m doubles each; either
+ * may be NULL; out_stride >= m when num_layers > 1).  Runs once eagerly, then ara_plan_launch replays it;
+ * results equal ara_pml_tvar_device bit for bit.  Errors: as ara_pml_tvar_device, plus ARA_E_CUDA when
+ * the graph cannot be captured. */
+ARA_API ara_status ara_metrics_plan_create(const double* ylt, uint64_t n, uint32_t num_layers, const double* rps,
+                                           uint32_t m, double* pml_dev, double* tvar_dev, uint64_t out_stride,
+                                           void* stream, ara_plan** out);
 
 /* End-to-end variant for a HOST YET (pinned memory gives copy/compute overlap; pageable works but
  * serialises): the YET is streamed to the device in trial batches on an internal copy stream,

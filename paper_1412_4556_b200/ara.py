@@ -38,7 +38,7 @@ EXPORTS = ("ara_create", "ara_destroy", "ara_run", "ara_run_ex", "ara_run_host",
            "ara_sum_layers", "ara_check", "ara_pml_tvar", "ara_pml",
            "ara_tvar", "ara_pml_tvar_device", "ara_table_footprint", "ara_unshard", "ara_set_option", "ara_get_option",
            "ara_layer_info", "ara_layer_stats", "ara_kernel_name", "ara_status_string", "ara_last_error",
-           "ara_version", "ara_plan_create", "ara_plan_launch", "ara_plan_destroy")
+           "ara_version", "ara_plan_create", "ara_plan_launch", "ara_plan_destroy", "ara_metrics_plan_create")
 
 
 class AraError(RuntimeError):
@@ -105,6 +105,7 @@ def lib() -> ctypes.CDLL:
             "ara_plan_create": (st, [vp, ctypes.POINTER(_Yet), dp, dp, u32, dp, dp, vp, ctypes.POINTER(vp)]),
             "ara_plan_launch": (st, [vp, vp]),
             "ara_plan_destroy": (None, [vp]),
+            "ara_metrics_plan_create": (st, [dp, u64, u32, dp, u32, dp, dp, u64, vp, ctypes.POINTER(vp)]),
             "ara_status_string": (ctypes.c_char_p, [ctypes.c_int]),
             "ara_last_error": (ctypes.c_char_p, []),
             "ara_version": (u32, []),
@@ -386,6 +387,19 @@ def ara_pml_tvar_device(ylt, rps: Sequence[float], pml_dev, tvar_dev, stream=Non
     n = _numel(ylt) if n is None else n
     _check(lib().ara_pml_tvar_device(_dptr(ylt), n, _dptr(r), r.size, _dptr(pml_dev), _dptr(tvar_dev),
                                      _stream_ptr(stream)), "ara_pml_tvar_device")
+
+
+def ara_metrics_plan_create(ylt, rps: Sequence[float], pml_dev=None, tvar_dev=None, out_stride: Optional[int] = None,
+                            stream=None) -> "Plan":
+    """Capture PML/TVaR of a device YLT [layers, n] (or [n]) as a CUDA graph (ara_metrics_plan_create); layer
+    l's results land at pml_dev / tvar_dev + l * out_stride (default m).  The tensors must outlive the plan."""
+    r = np.ascontiguousarray(rps, dtype=np.float64)
+    layers, n = (1, ylt.numel()) if ylt.dim() == 1 else (ylt.shape[0], ylt.shape[1])
+    h = ctypes.c_void_p()
+    _check(lib().ara_metrics_plan_create(_dptr(ylt), n, layers, _dptr(r), r.size, _dptr(pml_dev), _dptr(tvar_dev),
+                                         out_stride if out_stride is not None else r.size, _stream_ptr(stream),
+                                         ctypes.byref(h)), "ara_metrics_plan_create")
+    return Plan(h, (ylt, pml_dev, tvar_dev, r))
 
 
 def ara_pml(ylt, rps: Sequence[float], stream=None) -> np.ndarray:

@@ -1098,6 +1098,61 @@ ara_status ara_plan_launch(ara_plan* p, void* stream) {
 
 void ara_plan_destroy(ara_plan* p) { plan_free(p); }
 
+ara_status ara_metrics_plan_create(const double* ylt, uint64_t n, uint32_t num_layers, const double* rps, uint32_t m,
+                                   double* pml_dev, double* tvar_dev, uint64_t out_stride, void* stream,
+                                   ara_plan** out) {
+  if (!out) return set_error(ARA_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (!ylt || n == 0 || num_layers == 0 || !rps || m == 0 || (!pml_dev && !tvar_dev))
+    return set_error(ARA_E_ARG, "invalid metric plan arguments");
+  if (num_layers > 1 && out_stride < m) return set_error(ARA_E_ARG, "out_stride %llu < m", (unsigned long long)out_stride);
+  int dev = 0;
+  ARA_CUDA(cudaGetDevice(&dev));
+  cudaStream_t s = (cudaStream_t)stream;
+  ara_plan* p = new (std::nothrow) ara_plan();
+  if (!p) return set_error(ARA_E_NOMEM, "host allocation failed");
+  p->device = dev;
+  const size_t bytes = metrics_scratch_size(n);
+  if (cudaMalloc(&p->scratch, bytes) != cudaSuccess || cudaMemset(p->scratch, 0, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    plan_free(p);
+    return set_error(ARA_E_NOMEM, "metric scratch");
+  }
+  auto step = [&](cudaStream_t st) -> ara_status {
+    for (uint32_t l = 0; l < num_layers; ++l) {
+      const ara_status r = metrics_device_into(ylt + (uint64_t)l * n, n, rps, m, pml_dev ? pml_dev + l * out_stride : nullptr,
+                                               tvar_dev ? tvar_dev + l * out_stride : nullptr, p->scratch, bytes, st,
+                                               true);
+      if (r) return r;
+    }
+    return ARA_OK;
+  };
+  ara_status st = step(s);  // eager once: validates and sets the launch attributes outside the capture
+  if (st == ARA_OK && cudaStreamSynchronize(s) != cudaSuccess) st = cuda_error(cudaGetLastError(), "metric plan warm-up");
+  cudaStream_t cs = nullptr;
+  if (st == ARA_OK && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+    st = cuda_error(cudaGetLastError(), "capture stream");
+  if (st == ARA_OK) {
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      st = cuda_error(e, "cudaStreamBeginCapture");
+    } else {
+      st = step(cs);
+      e = cudaStreamEndCapture(cs, &p->graph);
+      if (st == ARA_OK && e != cudaSuccess) st = cuda_error(e, "cudaStreamEndCapture");
+      if (st == ARA_OK && (e = cudaGraphInstantiate(&p->exec, p->graph, 0)) != cudaSuccess)
+        st = cuda_error(e, "cudaGraphInstantiate");
+    }
+  }
+  if (cs) cudaStreamDestroy(cs);
+  if (st) {
+    plan_free(p);
+    return st;
+  }
+  *out = p;
+  return ARA_OK;
+}
+
 ara_status ara_check(ara_ctx* c, void* stream) {
   if (!c) return set_error(ARA_E_ARG, "ctx is NULL");
   DeviceGuard guard(c->device);

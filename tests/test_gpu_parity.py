@@ -531,6 +531,34 @@ def test_metrics_device_outputs_async(cuda_device):
         ara.ara_pml_tvar_device(ds[0], [n * 2.0], outs[0][0], None)
 
 
+def test_metrics_plan_replays_bitwise(cuda_device):
+    """ara_metrics_plan_create: a captured PML/TVaR step over three layers (> 16 return periods, strided
+    outputs as in a [layers][2][m] result block) equals the oracle bitwise, replay after replay, also after
+    the YLT is overwritten between launches (the graph reads the buffer, it caches nothing)."""
+    rng = np.random.default_rng(8)
+    L, n = 3, 300_000
+    rps = [2.0, 5.0, 10.0, 20.0, 25.0, 50.0, 100.0, 200.0, 250.0, 500.0, 1000.0, 2000.0, 5000.0, 10000.0,
+           20000.0, 50000.0, 100000.0, 7.5]
+    m = len(rps)
+    d = torch.empty((L, n), dtype=torch.float64, device="cuda")
+    out = torch.full((L, 2, m), -1.0, dtype=torch.float64, device="cuda")
+    d.copy_(torch.from_numpy(np.floor(rng.exponential(1e6, (L, n))) * (rng.random((L, n)) > 0.3)))
+    plan = ara.ara_metrics_plan_create(d, rps, out[:, 0], out[:, 1], out_stride=2 * m)
+    for it in range(3):
+        y = np.floor(rng.exponential(1e6 * (it + 1), (L, n))) * (rng.random((L, n)) > 0.3)
+        d.copy_(torch.from_numpy(y))
+        out.fill_(-1.0)
+        plan.launch()
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        for l in range(L):
+            assert np.array_equal(got[l, 0], oracle.pml(y[l], rps)), (it, l)
+            assert np.array_equal(got[l, 1], oracle.tvar(y[l], rps)), (it, l)
+    plan.close()
+    with pytest.raises(ara.AraError):
+        ara.ara_metrics_plan_create(d, rps, out[:, 0], out[:, 1], out_stride=m - 1)
+
+
 @pytest.mark.parametrize("layout", [ara.STUDY_INTERLEAVED, ara.STUDY_INDEPENDENT, ara.STUDY_SORTED, ara.STUDY_HASH,
                                     ara.STUDY_INDEX])
 def test_section_4b_study_layouts(cuda_device, layout):
