@@ -367,7 +367,8 @@ def main():
                                                stream=stream)
         ref_h = met_h.clone()
         met.zero_()
-        step()
+        mplan[0].launch(stream=stream)  # (not step(): a sharded step's gather is a collective of all ranks)
+        met_h.copy_(met, non_blocking=True)
         torch.cuda.synchronize()
         if not torch.equal(met_h, ref_h):
             print(json.dumps({"error": "captured metric step != ara_pml_tvar_device"}), flush=True)
