@@ -108,3 +108,22 @@ def test_gather_ylt_real_regime_vs_oracle(cuda_device, world, name, n):
     # the sharded run equals a single-process run bitwise (trial-local summation order)
     y1, pml1, tvar1, _ = _run(1, name, n)
     assert np.array_equal(y, y1) and np.array_equal(pml, pml1) and np.array_equal(tvar, tvar1)
+
+
+def test_bench_multi_rank_flow_completes(cuda_device):
+    """bench.py under torchrun with two ranks (gloo on the one GPU): the sharded step -- per-rank run,
+    YLT all-gather, PML/TVaR replayed on rank 0 -- completes and rank 0 prints one JSON line.  (A rank-0-only
+    replay of the whole step once ran the all-gather on one rank and hung the job.)"""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2", "--config",
+           "T", "--steps", "3", "--warmup", "3", "--dist-backend", "gloo", "--no-e2e", "--no-cpu-baseline", "--no-cold"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "error" not in d
