@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(kSelBlock) tail_pass(const double* __restrict_
 constexpr int kSelThreads = 1024;
 constexpr uint32_t kSelCache = 8192;      // cached keys per block (64 KB): n <= 8192 * SMs is read once
 constexpr uint32_t kSelHistWords = 32768; // 128 KB of packed u16 bin counters
-constexpr uint32_t kSelMapWords = 2048 + 512;  // 16-bit slot map: 65,536-bit presence + 2,048 u8 word bases
+constexpr uint32_t kSelMapWords = 2048 + 512 + 2048;  // first H pass: 65,536-bit prefix map + u8 word bases;
+                                                    // pass C: 65,536-bit map of the candidate buckets' prefixes
 constexpr uint32_t kSelSub = 65535;       // keys per histogram sub-chunk (a u16 counter cannot overflow)
 constexpr uint32_t kCandCap = 256;        // bucket size compacted instead of narrowed further
 constexpr int kSelMaxBlocks = 160;      // >= the SM count (148 on B200): one block per SM
@@ -416,14 +417,11 @@ __device__ __forceinline__ void build_slots(int mode, int m, const int* s_mode, 
     lo = s_pre[lane] << rb;
     hi = lo | ((1ull << rb) - 1ull);
   }
-  // distinct ranges: a query leads its range if no lower lane holds the same one
-  bool lead = in;
+  // distinct ranges: a query leads its range if no lower lane holds the same one (a range's lo is never ~0,
+  // the value every other lane holds)
+  const unsigned peers = __match_any_sync(0xffffffffu, lo);
+  const bool lead = in && (__ffs(peers) - 1) == lane;
   int rank = 0;  // number of distinct ranges below this one
-  for (int j = 0; j < m; ++j) {
-    const uint64_t lj = __shfl_sync(0xffffffffu, lo, j);
-    const bool inj = __shfl_sync(0xffffffffu, (int)in, j) != 0;
-    if (inj && lj == lo && j < lane) lead = false;
-  }
   const unsigned leaders = __ballot_sync(0xffffffffu, lead);
   for (int j = 0; j < m; ++j) {
     const uint64_t lj = __shfl_sync(0xffffffffu, lo, j);
@@ -447,6 +445,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
   uint64_t* skeys = sdyn;                                        // [kSelCache]
   uint32_t* hw = reinterpret_cast<uint32_t*>(sdyn + kSelCache);  // [kSelHistWords] packed u16 bins
   uint32_t* smap = hw + kSelHistWords;  // first H pass: bit d = 16-bit prefix d is a slot; then u8 bases
+  uint32_t* cmap = smap + 2560;         // pass C: bit d = 16-bit prefix d opens a candidate bucket
+  for (uint32_t i = threadIdx.x; i < 2048u; i += blockDim.x) cmap[i] = 0u;  // (visible after pass A's barriers)
   __shared__ uint64_t s_pre[kMaxQ], s_T[kMaxQ], s_up[kMaxQ], s_slo[kMaxQ], s_shi[kMaxQ];
   __shared__ uint32_t s_r[kMaxQ], s_above[kMaxQ];  // rank inside the bucket; keys above the bucket (or T)
   __shared__ int s_nbits[kMaxQ], s_mode[kMaxQ], s_q2slot[kMaxQ], s_nslot;
@@ -707,12 +707,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
     const int rb = 64 - s_nbits[q];
     s_up[q] = s_mode[q] == kModeDone ? s_T[q] : ((s_pre[q] << rb) | ((1ull << rb) - 1ull));
   }
-  for (uint32_t i = threadIdx.x; i < 2048u; i += blockDim.x) smap[i] = 0u;  // 16-bit prefixes of the buckets
   __syncthreads();
   const int nc = s_nslot;
   if (threadIdx.x < (unsigned)nc) {  // every candidate bucket holds >= 16 bits: its top 16 bits are one prefix
     const uint32_t d = (uint32_t)(s_slo[threadIdx.x] >> 48);
-    atomicOr(&smap[d >> 5], 1u << (d & 31u));
+    atomicOr(&cmap[d >> 5], 1u << (d & 31u));
   }
   __syncthreads();
   if (nc > 0) {  // block-local lists in shared memory, then copied to this block's region (no global atomics)
@@ -724,7 +723,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) metrics_select(const double* _
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
       const uint64_t key = key_at(i);
       const uint32_t d = (uint32_t)(key >> 48);
-      if (key >= rlo && key <= rhi && ((smap[d >> 5] >> (d & 31u)) & 1u)) {  // most keys stop at the map
+      if (key >= rlo && key <= rhi && ((cmap[d >> 5] >> (d & 31u)) & 1u)) {  // most keys stop at the map
         const int sl = find_range(key, s_slo, s_shi, nc);
         if (sl >= 0) lc[sl * kCandCap + atomicAdd(&s_ln[sl], 1u)] = key;
       }
